@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Benchmark: MTTKRP nnz·R/s and CP-ALS s/iter (fp64) — BASELINE.json metric.
+
+A *step* is one full pass of the hot path on one synthetic
+tensor already resident in HBM: splatt_cpd_als_ex = validate, COO->CSF build of every
+mode, factor init, `iters` CP-ALS iterations (Hadamard+Cholesky, MTTKRP, solve,
+normalise, Gram refresh, fit), finalise.  value = (N_modes * nnz * R * iters) per
+second of step time, summed over all ranks' shared work (whole-job throughput).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+
+N>1: launch under torchrun; the path is sharded by root slices with
+NCCL all-reduce / all-gather inside the library ("scaling": "strong", fixed tensor).
+--impl reference times the CPU oracle (the tier's reference arm) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+DEFAULT_CONFIG = "c2"  # BASELINE.json configs[1] (YELP-shaped), the metric's N=1 workload
+METRIC = "MTTKRP nnz·R/s and CP-ALS s/iter (fp64), % HBM roofline"
+UNIT = "nnz·R/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def algorithmic_units(cfg):
+    N = len(cfg["dims"])
+    return N * cfg["nnz"] * cfg["rank"] * cfg["iters"]
+
+
+def cpu_baseline(t, cfg, iters=2):
+    """The oracle as it stands, on the host cores, on a bounded sample (2 iterations)."""
+    import oracle
+    t0 = time.perf_counter()
+    r = oracle.cpd_als(t.dims, t.ind, t.vals, rank=cfg["rank"], max_iters=iters, tol=0.0,
+                       seed=cfg["seed"], timings=True)
+    wall = time.perf_counter() - t0
+    tm = r["timings"]
+    step = tm["loop"] + tm["sort"]
+    units = len(t.dims) * t.nnz * cfg["rank"] * iters
+    return {"value": units / step, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{cfg['name']} full tensor, {iters} of {cfg['iters']} CP-ALS iterations "
+                      f"(+ its per-mode grouping sort); wall {wall:.1f}s",
+            "sec_per_iter": tm["loop"] / iters,
+            "mttkrp_nnzR_per_s": len(t.dims) * t.nnz * cfg["rank"] * iters / tm["mttkrp"]}
+
+
+def run_reference(args, cfg, t):
+    """--impl reference: the CPU oracle (this tier's reference arm), rank 0 only."""
+    import oracle
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    iters = 1
+    units = len(t.dims) * t.nnz * cfg["rank"] * iters
+    for _ in range(args.warmup):
+        oracle.cpd_als(t.dims, t.ind, t.vals, rank=cfg["rank"], max_iters=iters, seed=cfg["seed"])
+    times = []
+    for _ in range(args.steps):
+        r = oracle.cpd_als(t.dims, t.ind, t.vals, rank=cfg["rank"], max_iters=iters,
+                           seed=cfg["seed"], timings=True)
+        times.append(r["timings"]["loop"] + r["timings"]["sort"])
+    tot = sum(times)
+    value = units * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(cfg, args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(),
+                         "kind": "oracle",
+                         "sample": f"{cfg['name']} full tensor, {iters} CP-ALS iteration per step "
+                                   "(+ per-mode grouping sort)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(cfg, G):
+    return {"workload": cfg["name"], "dims": list(cfg["dims"]), "nnz": cfg["nnz"],
+            "rank": cfg["rank"], "iters": cfg["iters"], "seed": cfg["seed"],
+            "parallelism": f"slice-partitioned x{G}" if G > 1 else "single GPU",
+            "l2": "inputs larger than L2 (COO + per-mode CSFs >> 126 MB); no explicit flush"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=DEFAULT_CONFIG)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--iters", type=int, default=None, help="override CP-ALS iterations")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    import synth
+    cfg = dict(synth.config(args.config))
+    cfg["name"] = args.config
+    if args.iters:
+        cfg["iters"] = args.iters
+    t0 = time.perf_counter()
+    t = synth.generate_config(args.config)
+    log(f"[bench] generated {args.config}: dims={t.dims} nnz={t.nnz} in "
+        f"{time.perf_counter() - t0:.1f}s")
+
+    if args.impl == "reference":
+        run_reference(args, cfg, t)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1812_05961_b200 as sb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    stream = torch.cuda.Stream(local)
+    ctx = sb.Context(local, stream=stream)
+    if world > 1:
+        ctx.set_comm()
+
+    N = len(t.dims)
+    R, iters = cfg["rank"], cfg["iters"]
+    with torch.cuda.stream(stream):
+        ind = [torch.from_numpy(a.view(np.int32)).cuda(local) for a in t.ind]
+        vals = torch.from_numpy(t.vals).cuda(local)
+    torch.cuda.synchronize(local)
+
+    def step(stats=True):
+        return sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=iters, tol=0.0,
+                          seed=cfg["seed"], ctx=ctx, stats=stats)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(local)
+    if world > 1:
+        dist.barrier()
+
+    runs = []
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(local)
+        if world > 1:
+            dist.barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            runs.append(step())
+        ev1.record(stream)
+        torch.cuda.synchronize(local)
+        if world > 1:
+            dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+
+    # ---------------------------------------------------------------- e2e
+    e2e = None
+    if not args.no_e2e:
+        pin_ind = [torch.from_numpy(a.view(np.int32)).pin_memory() for a in t.ind]
+        pin_val = torch.from_numpy(t.vals).pin_memory()
+        h_ind = [p.numpy() for p in pin_ind]
+        h_val = pin_val.numpy()
+        e_times = []
+        for k in range(max(1, args.steps // 2) + 1):
+            torch.cuda.synchronize(local)
+            a = time.perf_counter()
+            r = sb.cpd_als(h_ind, h_val, t.dims, rank=R, max_iters=iters, seed=cfg["seed"],
+                           ctx=ctx, out_device=False)
+            b = time.perf_counter()
+            if k > 0:
+                e_times.append(b - a)
+        emax = max(e_times) if world == 1 else e_times
+        et = float(np.mean(e_times))
+        if world > 1:
+            tt = torch.tensor([et], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            et = float(tt.item())
+        h2d = t.nnz * (4 * N + 8)
+        d2h = sum(int(d) for d in t.dims) * R * 8 + R * 8
+        e2e = {"value": algorithmic_units(cfg) / et, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "sec_per_step": et,
+               "note": "public API sb.cpd_als with pinned host COO in, host factors out; "
+                       "H2D/D2H inside the timed call"}
+        del emax
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ------------------------------------------------------------- summarise
+    st = [r["stats"] for r in runs]
+    t_mttkrp = sum(s["t_mttkrp"] for s in st)
+    alg_bytes = sum(s["mttkrp_alg_bytes"] for s in st)
+    launches = sum(s["mttkrp_launches"] for s in st)
+    peak, peak_src = peaks()
+    achieved = alg_bytes / t_mttkrp / 1e9 if t_mttkrp > 0 else 0.0
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "mttkrp_traffic.json")
+    if os.path.exists(tf):
+        try:
+            with open(tf) as f:
+                d = json.load(f).get(f"{args.config}:G{world}")
+            traffic = d and d.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    units = algorithmic_units(cfg) * args.steps
+    value = units / (ms * 1e-3)
+    loop = [s["t_loop"] for s in st]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(cfg, world),
+        "cpals_sec_per_iter": statistics.mean(loop) / iters,
+        "mttkrp_nnzR_per_s": N * t.nnz * R * iters * args.steps / t_mttkrp if t_mttkrp else None,
+        "breakdown_s_per_step": {k: sum(s[k] for s in st) / args.steps for k in
+                                 ("t_build", "t_mttkrp", "t_inverse", "t_ata", "t_norm", "t_fit",
+                                  "t_comm", "t_loop")},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "mttkrp_root_kernel", "peak_source": peak_src,
+                     "alg_bytes_per_launch": alg_bytes / max(1, launches),
+                     "avg_launch_ms": 1e3 * t_mttkrp / max(1, launches),
+                     "launches": launches},
+        "gpu_launches": sum(s["kernel_launches"] for s in st),
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(t, cfg)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

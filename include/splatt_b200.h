@@ -1,0 +1,193 @@
+/*
+ * splatt_b200.h — C ABI of the B200-native sparse CP-ALS hot path.
+ *
+ * The method: CP-ALS (Algorithm 1) over CSF-compressed sparse
+ * tensors, whose dominant step is the per-mode MTTKRP
+ * M_n = X_(n) (KRP_{m != n} A_m)  (lines 5/8/11).
+ * The calls follow the problem statement of BASELINE.json's north star:
+ *   splatt_csf_build(coo, nmodes, dims), splatt_mttkrp(csf, mode, factors, out),
+ *   splatt_cpd_als(coo, rank, max_iters, tol, seed) -> factors, lambda, fit.
+ * Readings of passages the paper leaves open are listed in DESIGN.md §2.
+ *
+ * Conventions (every call):
+ *  - Every function returns splatt_status (0 = OK) unless noted.  On error the
+ *    context keeps a message (splatt_last_error).  No call throws or aborts.
+ *  - Argument errors are detected synchronously, before any device work.
+ *  - Indices are 0-based uint32; values and factors are fp64.
+ *  - Factor / output matrices are row-major I_n x R with a leading dimension ld
+ *    (elements between consecutive rows), ld >= R.
+ *  - Ownership: the caller owns every pointer it passes (COO arrays, factors,
+ *    outputs); the library never frees caller memory.  The library owns
+ *    splatt_ctx (free with splatt_ctx_destroy) and splatt_csf (splatt_csf_free).
+ *  - Memory spaces: splatt_csf_build and splatt_cpd_als accept host OR device
+ *    pointers for the COO and the outputs (detected with cudaPointerGetAttributes;
+ *    host buffers are copied inside the call).  splatt_mttkrp takes device
+ *    pointers only.
+ *  - Streams: every device operation is ordered on the context stream (the one
+ *    passed to splatt_ctx_create, else the library's own).  splatt_csf_build and
+ *    splatt_mttkrp return after enqueueing (asynchronous faults surface as
+ *    SPLATT_ERR_CUDA from a later call or splatt_ctx_sync); splatt_cpd_als
+ *    returns when its outputs are written.
+ *  - Threading: one context per host thread; distinct contexts are independent.
+ *  - No CPU fallback exists: every arithmetic step runs in the library's CUDA
+ *    kernels on the context's device.
+ */
+#ifndef SPLATT_B200_H
+#define SPLATT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SPLATT_OK = 0,
+  SPLATT_ERR_BADINPUT = -1,    /* invalid argument (see each call)                       */
+  SPLATT_ERR_NOMEM = -2,       /* device or host allocation failed                      */
+  SPLATT_ERR_SINGULAR = -3,    /* Cholesky of V failed after the ridge retry (C-7)      */
+  SPLATT_ERR_CUDA = -4,        /* CUDA runtime error (message in splatt_last_error)     */
+  SPLATT_ERR_NCCL = -5,        /* NCCL error or NCCL library not loadable               */
+  SPLATT_ERR_EMPTY = -6,       /* ||X|| = 0: the fit is undefined         */
+  SPLATT_ERR_UNSUPPORTED = -7  /* valid but outside this build (e.g. nnz >= 2^32)       */
+} splatt_status;
+
+enum { SPLATT_MAX_NMODES = 8, SPLATT_MAX_RANK = 128 };
+
+/* CSF allocation policy.  ALL: one CSF rooted at every mode, so
+ * every MTTKRP is a root ("no-lock") traversal.                       */
+enum { SPLATT_CSF_ALL = 0 };
+
+typedef struct splatt_ctx splatt_ctx;   /* device, stream, allocator pool, optional comm */
+typedef struct splatt_csf splatt_csf;   /* device-resident CSF set, immutable after build */
+
+/* Sparse tensor in coordinate form (SoA).  nmodes in [3, 8]; nnz >= 1;
+ * dims[m] in [1, 2^32); ind[m][p] < dims[m]; duplicates are kept as distinct
+ * adjacent leaves in input order.                                 */
+typedef struct {
+  int32_t         nmodes;
+  uint64_t        nnz;
+  uint64_t        dims[SPLATT_MAX_NMODES];
+  const uint32_t* ind[SPLATT_MAX_NMODES];
+  const double*   vals;
+} splatt_coo;
+
+/* Caller-allocated CP-ALS outputs (Alg. 1 line 14).                */
+typedef struct {
+  double*  factors[SPLATT_MAX_NMODES]; /* I_n x R, row-major, ld = R; host or device      */
+  double*  lambda;                     /* R weights; host or device                        */
+  double   fit;                        /* fit after the last iteration (C-10)              */
+  int32_t  iters;                      /* iterations executed                              */
+  double*  fit_history;                /* optional (NULL): max_iters doubles, host memory  */
+} splatt_kruskal;
+
+/* Per-call measurements, filled by splatt_cpd_als_ex when non-NULL.  Times are
+ * seconds from CUDA events on the context stream, summed over the call, in the
+ * categories of Table III plus COMM; counters are exact.            */
+typedef struct {
+  double   t_mttkrp;        /* all MTTKRP launches (incl. output zeroing)               */
+  double   t_build;         /* validation + COO->CSF build ("Sort")                     */
+  double   t_ata;           /* Hadamard of Grams + Gram refresh ("Mat A^TA")           */
+  double   t_norm;          /* lambda + column scaling ("Mat norm")                     */
+  double   t_fit;           /* fit ("CPD fit")                                          */
+  double   t_inverse;       /* Cholesky + row solves ("Inverse")                        */
+  double   t_comm;          /* NCCL collectives (0 on one GPU)                          */
+  double   t_loop;          /* whole ALS loop (all iterations)                          */
+  double   mttkrp_alg_bytes;/* sum over launches of the algorithmic bytes B_alg(n)     */
+  uint64_t mttkrp_launches; /* MTTKRP kernel launches                                   */
+  uint64_t kernel_launches; /* every library kernel launched by the call                */
+  uint64_t csf_nodes[SPLATT_MAX_NMODES][SPLATT_MAX_NMODES]; /* [csf][level] local nodes */
+  int32_t  iters;
+  int32_t  nranks;
+} splatt_stats;
+
+/* ---------------------------------------------------------------- context */
+/* Create a context on CUDA device `device`.  cuda_stream: a cudaStream_t to order
+ * all work on (e.g. torch.cuda.current_stream().cuda_stream), or NULL for a
+ * library-owned non-blocking stream.  *out is set only on success.              */
+splatt_status splatt_ctx_create(splatt_ctx** out, int device, void* cuda_stream);
+void          splatt_ctx_destroy(splatt_ctx* ctx);
+/* Wait for all work on the context stream; reports asynchronous faults.         */
+splatt_status splatt_ctx_sync(splatt_ctx* ctx);
+/* Last error message of this context ("" if none); valid until the next call.   */
+const char*   splatt_last_error(const splatt_ctx* ctx);
+const char*   splatt_version(void);
+
+/* ------------------------------------------------- multi-GPU (one process per GPU)
+ * every rank passes the same full COO; nonzeros are partitioned by
+ * root slices of each mode's CSF (splatt_partition), each rank owns the output rows
+ * of its slice range, updated factor rows are all-gathered and the R x R Grams,
+ * column maxima and the fit inner product are all-reduced with NCCL.
+ * splatt_comm_unique_id: rank 0 only; writes 128 bytes (ncclUniqueId), to be
+ * broadcast by the caller (e.g. torch.distributed).  splatt_ctx_set_comm: collective
+ * over the nranks ranks (ncclCommInitRank).  NCCL is loaded at run time
+ * (libnccl.so.2); failure -> SPLATT_ERR_NCCL.                                      */
+splatt_status splatt_comm_unique_id(void* id128);
+splatt_status splatt_ctx_set_comm(splatt_ctx* ctx, const void* id128, int nranks, int rank);
+
+/* Host-only (no device needed): cut S slices with nnz weights w[0..S) into G
+ * contiguous ranges minimising the maximum range weight;
+ * boundaries leftmost-greedy under the optimal cap.  bounds: G+1 entries,
+ * bounds[0] = 0, bounds[G] = S.  G >= 1.                                          */
+splatt_status splatt_partition(const uint64_t* w, uint64_t S, int32_t G, uint64_t* bounds);
+
+/* ---------------------------------------------------------------- CSF */
+/* Build the CSF set of `coo` on the device (sort = PAPER.md:415).
+ * CSF_n (policy ALL) is rooted at mode n; below the root the other modes follow by
+ * ascending length, ties to the lower mode id.  Level l < N-1
+ * holds ids_l (the level's coordinate) and ptr_l (offsets into level l+1, one
+ * extra end entry); the leaf level holds ids_{N-1} and vals in sorted order.
+ * Bit-exact: the result is a pure integer function of the input.
+ * nmodes and dims must equal coo->nmodes / coo->dims (they follow the north star's
+ * call shape).  Errors: BADINPUT (nmodes, nnz = 0, dims, index >= dim, unknown
+ * policy, mismatch), UNSUPPORTED (nnz >= 2^32).                                     */
+splatt_status splatt_csf_build(splatt_ctx* ctx, const splatt_coo* coo, int32_t nmodes,
+                               const uint64_t* dims, int32_t policy, splatt_csf** out);
+/* Shape of CSF `which` (0..ncsf-1): mode_perm[0..N) (level -> mode) and n_nodes[l]
+ * per level; either may be NULL.  Synchronous, host outputs.                       */
+splatt_status splatt_csf_info(const splatt_csf* csf, int32_t which, int32_t* nmodes,
+                              int32_t* mode_perm, uint64_t* n_nodes);
+/* Copy level `level` of CSF `which` to HOST buffers (any may be NULL): ids
+ * (n_nodes[level]), ptr (n_nodes[level]+1; levels < N-1 only), vals (nnz; leaf
+ * level only).  Synchronous.  For bit-exact tests.                                 */
+splatt_status splatt_csf_export(const splatt_csf* csf, int32_t which, int32_t level,
+                                uint32_t* ids, uint32_t* ptr, double* vals);
+void          splatt_csf_free(splatt_csf* csf);
+
+/* ---------------------------------------------------------------- MTTKRP */
+/* out[i, r] = sum over nonzeros p with ind_mode[p] = i of
+ *             v_p * prod_{m != mode} factors[m][ind_m[p] * ld + r]      (C-6)
+ * for every i < dims[mode], r < rank; rows with no nonzeros are written 0; columns
+ * r >= rank of `out` are written 0.  factors: N device pointers (factors[mode] is
+ * ignored, may be NULL), each dims[m] x ld.  out: device, dims[mode] x ld.
+ * Uses the CSF rooted at `mode`.  Errors: BADINPUT (mode, rank not in [1,128],
+ * ld < rank, NULL pointers).  Asynchronous on the context stream.                  */
+splatt_status splatt_mttkrp(splatt_ctx* ctx, const splatt_csf* csf, int32_t mode,
+                            const double* const* factors, int32_t rank, int32_t ld,
+                            double* out);
+
+/* ---------------------------------------------------------------- CP-ALS */
+/* Algorithm 1 for an N-mode tensor, fixed readings DESIGN.md §2:
+ * factors initialised U[0,1) by counter-based splitmix64 from `seed` (C-2); per
+ * iteration, per mode n: V = *_{m!=n} G_m, M = MTTKRP_n, A_n = M V^-1 by Cholesky
+ * (ridge retry, C-7), column norms into lambda (2-norm in iteration 1, max(1,|.|max)
+ * later, C-8), Gram refresh; then the fit (C-10); stop when it >= 2 and
+ * |fit - fit_prev| < tol, or at max_iters (tol = 0: exactly max_iters).  Returned
+ * factors have unit 2-norm columns with the norms folded into lambda (C-12).
+ * Errors: BADINPUT (as csf_build; rank not in [1,128]; max_iters < 1; tol < 0 or
+ * NaN), EMPTY (||X|| = 0), SINGULAR.  Synchronous.                                  */
+splatt_status splatt_cpd_als(splatt_ctx* ctx, const splatt_coo* coo, int32_t rank,
+                             int32_t max_iters, double tol, uint64_t seed,
+                             splatt_kruskal* out);
+/* As splatt_cpd_als, plus: init_factors (NULL = seeded init; else N pointers,
+ * host or device, I_n x rank, ld = rank, used as the initial A_n), policy
+ * (SPLATT_CSF_ALL), stats (NULL or filled; see splatt_stats).                      */
+splatt_status splatt_cpd_als_ex(splatt_ctx* ctx, const splatt_coo* coo, int32_t rank,
+                                int32_t max_iters, double tol, uint64_t seed,
+                                const double* const* init_factors, int32_t policy,
+                                splatt_kruskal* out, splatt_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPLATT_B200_H */

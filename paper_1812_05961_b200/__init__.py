@@ -1,0 +1,361 @@
+"""paper_1812_05961_b200 — B200-native sparse CP-ALS hot path (arXiv 1812.05961).
+
+Thin ctypes binding of ``libsplatt_b200.so`` (C ABI: ``include/splatt_b200.h``).
+Argument marshalling only: every step of the method (CSF build, MTTKRP, Gram,
+Hadamard, Cholesky solve, normalisation, fit) runs in the library's sm_100a CUDA
+kernels.  There is no CPU fallback: if the shared library is missing or no CUDA
+device is present, calls raise.
+
+    ctx = Context()                                   # device 0, torch's current stream
+    csf = csf_build(ind, vals, dims, ctx=ctx)         # splatt_csf_build
+    M = mttkrp(csf, mode, factors, ctx=ctx)           # splatt_mttkrp
+    res = cpd_als(ind, vals, dims, rank=35, max_iters=20, tol=0.0, seed=2)   # splatt_cpd_als
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+__all__ = ["lib", "Context", "Csf", "csf_build", "mttkrp", "cpd_als", "partition",
+           "SplattError", "SingularError", "EmptyTensorError", "STATUS", "padded_ld"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsplatt_b200.so")
+MAX_NMODES = 8
+MAX_RANK = 128
+
+STATUS = {0: "OK", -1: "BADINPUT", -2: "NOMEM", -3: "SINGULAR", -4: "CUDA", -5: "NCCL",
+          -6: "EMPTY", -7: "UNSUPPORTED"}
+
+
+class SplattError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"splatt {STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class SingularError(SplattError, ArithmeticError):
+    pass
+
+
+class EmptyTensorError(SplattError, ValueError):
+    pass
+
+
+class BadInputError(SplattError, ValueError):
+    pass
+
+
+class Coo(C.Structure):
+    _fields_ = [("nmodes", C.c_int32), ("nnz", C.c_uint64), ("dims", C.c_uint64 * MAX_NMODES),
+                ("ind", C.c_void_p * MAX_NMODES), ("vals", C.c_void_p)]
+
+
+class Kruskal(C.Structure):
+    _fields_ = [("factors", C.c_void_p * MAX_NMODES), ("lambda_", C.c_void_p),
+                ("fit", C.c_double), ("iters", C.c_int32), ("fit_history", C.c_void_p)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("t_mttkrp", C.c_double), ("t_build", C.c_double), ("t_ata", C.c_double),
+                ("t_norm", C.c_double), ("t_fit", C.c_double), ("t_inverse", C.c_double),
+                ("t_comm", C.c_double), ("t_loop", C.c_double),
+                ("mttkrp_alg_bytes", C.c_double), ("mttkrp_launches", C.c_uint64),
+                ("kernel_launches", C.c_uint64),
+                ("csf_nodes", (C.c_uint64 * MAX_NMODES) * MAX_NMODES),
+                ("iters", C.c_int32), ("nranks", C.c_int32)]
+
+    def to_dict(self, nmodes=None):
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "csf_nodes"}
+        n = nmodes or MAX_NMODES
+        d["csf_nodes"] = [[int(self.csf_nodes[i][l]) for l in range(n)] for i in range(n)]
+        return d
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def lib():
+    """Load libsplatt_b200.so (built in-tree by ``paper_1812_05961_b200.build``)."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1812_05961_b200.build`"
+                                  " (no CPU fallback exists)")
+            L = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+            P, i32, u64, f64 = C.c_void_p, C.c_int32, C.c_uint64, C.c_double
+            st = C.c_int
+            sig = {
+                "splatt_version": (C.c_char_p, []),
+                "splatt_ctx_create": (st, [C.POINTER(P), C.c_int, P]),
+                "splatt_ctx_destroy": (None, [P]),
+                "splatt_ctx_sync": (st, [P]),
+                "splatt_last_error": (C.c_char_p, [P]),
+                "splatt_comm_unique_id": (st, [P]),
+                "splatt_ctx_set_comm": (st, [P, P, C.c_int, C.c_int]),
+                "splatt_partition": (st, [P, u64, i32, P]),
+                "splatt_csf_build": (st, [P, C.POINTER(Coo), i32, P, i32, C.POINTER(P)]),
+                "splatt_csf_info": (st, [P, i32, C.POINTER(i32), P, P]),
+                "splatt_csf_export": (st, [P, i32, i32, P, P, P]),
+                "splatt_csf_free": (None, [P]),
+                "splatt_mttkrp": (st, [P, P, i32, P, i32, i32, P]),
+                "splatt_cpd_als": (st, [P, C.POINTER(Coo), i32, i32, f64, u64, C.POINTER(Kruskal)]),
+                "splatt_cpd_als_ex": (st, [P, C.POINTER(Coo), i32, i32, f64, u64, P, i32,
+                                           C.POINTER(Kruskal), C.POINTER(Stats)]),
+            }
+            for name, (res, args) in sig.items():
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+    return _lib
+
+
+def _raise(code, ctx_ptr=None):
+    if code == 0:
+        return
+    msg = lib().splatt_last_error(ctx_ptr)
+    msg = msg.decode() if msg else ""
+    cls = {-1: BadInputError, -3: SingularError, -6: EmptyTensorError}.get(code, SplattError)
+    raise cls(code, msg)
+
+
+def padded_ld(rank: int) -> int:
+    return (rank + 3) // 4 * 4
+
+
+def _ptr(x):
+    """Raw address of a torch tensor or numpy array (no copy; caller keeps it alive)."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()
+
+
+class Context:
+    """splatt_ctx: a device, a stream (torch's current stream by default), a comm."""
+
+    def __init__(self, device: int = 0, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("no CUDA device: the B200 path has no CPU fallback")
+        self.device = int(device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        p = C.c_void_p()
+        _raise(lib().splatt_ctx_create(C.byref(p), self.device, C.c_void_p(handle)))
+        self._p = p
+        self.nranks, self.rank = 1, 0
+
+    @property
+    def ptr(self):
+        return self._p
+
+    def sync(self):
+        _raise(lib().splatt_ctx_sync(self._p), self._p)
+
+    def set_comm(self, group=None):
+        """Create the NCCL communicator of this rank from a torch.distributed group."""
+        import torch.distributed as dist
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        buf = (C.c_char * 128)()
+        if rank == 0:
+            _raise(lib().splatt_comm_unique_id(buf))
+        obj = [bytes(buf)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        raw = (C.c_char * 128).from_buffer_copy(obj[0])
+        _raise(lib().splatt_ctx_set_comm(self._p, raw, world, rank), self._p)
+        self.nranks, self.rank = world, rank
+
+    def close(self):
+        if getattr(self, "_p", None):
+            lib().splatt_ctx_destroy(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default_ctx:
+        _default_ctx[device] = Context(device)
+    return _default_ctx[device]
+
+
+def _make_coo(ind, vals, dims):
+    N = len(dims)
+    if N != len(ind):
+        raise ValueError("len(ind) must equal len(dims)")
+    if N < 1 or N > MAX_NMODES:
+        raise ValueError("nmodes must be in [3, 8]")
+    coo = Coo()
+    coo.nmodes = N
+    coo.nnz = int(vals.shape[0])
+    for m in range(N):
+        coo.dims[m] = int(dims[m])
+        if int(ind[m].shape[0]) != coo.nnz:
+            raise ValueError("every ind[m] must have nnz entries")
+        coo.ind[m] = _ptr(ind[m])
+    coo.vals = _ptr(vals)
+    return coo
+
+
+def _as_u32(a):
+    if isinstance(a, np.ndarray):
+        return np.ascontiguousarray(a, dtype=np.uint32)
+    import torch
+    if a.dtype == torch.int32 or a.dtype == torch.uint32:
+        return a.contiguous()
+    raise TypeError("index tensors must be uint32/int32 (uint32 semantics)")
+
+
+def _as_f64(a):
+    if isinstance(a, np.ndarray):
+        return np.ascontiguousarray(a, dtype=np.float64)
+    import torch
+    if a.dtype != torch.float64:
+        raise TypeError("values must be float64")
+    return a.contiguous()
+
+
+class Csf:
+    """Handle to a device-resident CSF set (splatt_csf)."""
+
+    def __init__(self, p, ctx, dims):
+        self._p = p
+        self.ctx = ctx
+        self.dims = tuple(int(d) for d in dims)
+
+    def info(self, which: int):
+        n = C.c_int32()
+        perm = np.zeros(MAX_NMODES, dtype=np.int32)
+        nodes = np.zeros(MAX_NMODES, dtype=np.uint64)
+        _raise(lib().splatt_csf_info(self._p, which, C.byref(n), perm.ctypes.data, nodes.ctypes.data),
+               self.ctx.ptr)
+        return perm[: n.value].tolist(), nodes[: n.value].astype(np.int64).tolist()
+
+    def export(self, which: int):
+        """All levels of CSF `which` as host numpy arrays: dict(perm, ids, ptr, vals)."""
+        perm, nodes = self.info(which)
+        N = len(perm)
+        ids, ptr = [], []
+        vals = np.empty(nodes[N - 1], dtype=np.float64)
+        for l in range(N):
+            a = np.empty(nodes[l], dtype=np.uint32)
+            b = np.empty(nodes[l] + 1, dtype=np.uint32) if l < N - 1 else None
+            _raise(lib().splatt_csf_export(self._p, which, l, a.ctypes.data,
+                                           b.ctypes.data if b is not None else None,
+                                           vals.ctypes.data if l == N - 1 else None), self.ctx.ptr)
+            ids.append(a)
+            if b is not None:
+                ptr.append(b)
+        return dict(perm=perm, ids=ids, ptr=ptr, vals=vals)
+
+    def free(self):
+        if getattr(self, "_p", None):
+            lib().splatt_csf_free(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def csf_build(ind, vals, dims, ctx: Context | None = None, policy: int = 0) -> Csf:
+    """splatt_csf_build: one CSF per mode (policy ALL).  ind/vals host or device."""
+    ctx = ctx or default_context()
+    ind = [_as_u32(a) for a in ind]
+    vals = _as_f64(vals)
+    coo = _make_coo(ind, vals, dims)
+    d = (C.c_uint64 * MAX_NMODES)(*[int(x) for x in dims])
+    p = C.c_void_p()
+    _raise(lib().splatt_csf_build(ctx.ptr, C.byref(coo), len(dims), d, policy, C.byref(p)), ctx.ptr)
+    return Csf(p, ctx, dims)
+
+
+def mttkrp(csf: Csf, mode: int, factors, out=None, rank: int | None = None):
+    """splatt_mttkrp.  factors: list of N float64 CUDA tensors (I_m x ld, row-major);
+    factors[mode] may be None.  Returns out (I_mode x ld)."""
+    import torch
+    ctx = csf.ctx
+    ref = next(f for m, f in enumerate(factors) if m != mode and f is not None)
+    ld = int(ref.stride(0))
+    R = int(rank if rank is not None else ref.shape[1])
+    if out is None:
+        out = torch.empty((csf.dims[mode], ld), dtype=torch.float64, device=ref.device)
+    arr = (C.c_void_p * len(factors))(*[(_ptr(f) if f is not None and m != mode else None)
+                                        for m, f in enumerate(factors)])
+    _raise(lib().splatt_mttkrp(ctx.ptr, csf._p, mode, arr, R, int(out.stride(0)), _ptr(out)),
+           ctx.ptr)
+    return out
+
+
+def cpd_als(ind, vals, dims, rank: int, max_iters: int, tol: float = 0.0, seed: int = 0,
+            init=None, ctx: Context | None = None, out_device: bool = True, stats: bool = False):
+    """splatt_cpd_als(_ex).  Returns dict(factors, lam, fit, iters, fit_history[, stats]).
+
+    ind/vals may be host (numpy / CPU tensors) or CUDA tensors; outputs are CUDA
+    tensors if out_device else numpy arrays."""
+    import torch
+    ctx = ctx or default_context()
+    ind = [_as_u32(a) if not (hasattr(a, "is_cuda") and not a.is_cuda) else _as_u32(a.numpy())
+           for a in ind]
+    vals = _as_f64(vals.numpy() if hasattr(vals, "is_cuda") and not vals.is_cuda else vals)
+    coo = _make_coo(ind, vals, dims)
+    N = len(dims)
+    if out_device:
+        fac = [torch.empty((int(d), rank), dtype=torch.float64, device=f"cuda:{ctx.device}")
+               for d in dims]
+        lam = torch.empty(rank, dtype=torch.float64, device=f"cuda:{ctx.device}")
+    else:
+        fac = [np.empty((int(d), rank)) for d in dims]
+        lam = np.empty(rank)
+    hist = np.zeros(max(1, max_iters))
+    kr = Kruskal()
+    for m in range(N):
+        kr.factors[m] = _ptr(fac[m])
+    kr.lambda_ = _ptr(lam)
+    kr.fit_history = hist.ctypes.data
+    init_arr = None
+    if init is not None:
+        init = [np.ascontiguousarray(a, dtype=np.float64) if isinstance(a, np.ndarray)
+                else a.contiguous() for a in init]
+        init_arr = (C.c_void_p * N)(*[_ptr(a) for a in init])
+    st = Stats() if stats else None
+    code = lib().splatt_cpd_als_ex(ctx.ptr, C.byref(coo), rank, max_iters, float(tol), int(seed),
+                                   init_arr, 0, C.byref(kr), C.byref(st) if st else None)
+    _raise(code, ctx.ptr)
+    res = dict(factors=fac, lam=lam, fit=kr.fit, iters=kr.iters,
+               fit_history=hist[: kr.iters].copy())
+    if st is not None:
+        res["stats"] = st.to_dict(N)
+    return res
+
+
+def partition(weights, G: int):
+    """splatt_partition (host-only, C-14): optimal contiguous split of slice weights."""
+    w = np.ascontiguousarray(np.asarray(weights, dtype=np.uint64))
+    b = np.zeros(G + 1, dtype=np.uint64)
+    _raise(lib().splatt_partition(w.ctypes.data if w.size else None, w.shape[0], G, b.ctypes.data))
+    return b.astype(np.int64)
+
+
+def version() -> str:
+    return lib().splatt_version().decode()

@@ -1,0 +1,297 @@
+// als.cu — the CP-ALS driver (Algorithm 1).
+//
+// Host loop over iterations and modes; every step is a kernel on the context stream,
+// there is no host round trip inside an iteration (the only device->host read per
+// iteration is the fit, and only when tol > 0).  With a communicator the path is
+// sharded: per mode the root slices are cut into contiguous ranges
+// balanced on nnz (C-14), each rank builds the CSF of its own nonzeros, solves its own
+// rows, and the Gram/inner/colmax statistics and the updated rows are exchanged.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "als.hpp"
+#include "csf.hpp"
+#include "dense.hpp"
+#include "mttkrp.hpp"
+
+namespace sb {
+
+namespace {
+
+enum Cat { kMttkrp = 0, kBuild, kAta, kNorm, kFit, kInverse, kComm, kLoop, kNumCat };
+
+__global__ void histogram_kernel(const uint32_t* __restrict__ ind, uint64_t nnz,
+                                 unsigned long long* __restrict__ cnt) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
+       j += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[ind[j]], 1ull);
+}
+
+__global__ void owned_flags_kernel(const uint32_t* __restrict__ ind, uint64_t nnz, uint32_t lo,
+                                   uint32_t hi, uint32_t* __restrict__ flag) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
+       j += (uint64_t)gridDim.x * blockDim.x)
+    flag[j] = (ind[j] >= lo && ind[j] < hi) ? 1u : 0u;
+}
+
+struct Compact {
+  const uint32_t* src[SPLATT_MAX_NMODES];
+  uint32_t* dst[SPLATT_MAX_NMODES];
+  int N;
+};
+
+// Stable compaction: flag[j] (0/1) and its exclusive scan pos[j].
+__global__ void compact_kernel(Compact c, const double* __restrict__ vin, double* __restrict__ vout,
+                               const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
+                               uint64_t nnz) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    if (flag[j]) {
+      const uint32_t k = pos[j];
+      for (int m = 0; m < c.N; ++m) c.dst[m][k] = c.src[m][j];
+      vout[k] = vin[j];
+    }
+  }
+}
+
+int blocks_for(splatt_ctx* ctx, uint64_t n) {
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(n, 256), (uint64_t)ctx->num_sms * 16));
+}
+
+}  // namespace
+
+void host_partition(const uint64_t* w, uint64_t S, int G, uint64_t* bounds) {
+  // C-14 reading: smallest feasible cap by bisection, then
+  // leftmost-greedy boundaries under it.
+  auto feasible = [&](uint64_t cap) {
+    int parts = 1;
+    uint64_t cur = 0;
+    for (uint64_t s = 0; s < S; ++s) {
+      if (w[s] > cap) return false;
+      if (cur + w[s] > cap) { ++parts; cur = 0; }
+      cur += w[s];
+    }
+    return parts <= G;
+  };
+  uint64_t lo = 0, hi = 0;
+  for (uint64_t s = 0; s < S; ++s) { lo = std::max(lo, w[s]); hi += w[s]; }
+  while (lo < hi) {
+    const uint64_t mid = lo + (hi - lo) / 2;
+    if (feasible(mid)) hi = mid; else lo = mid + 1;
+  }
+  uint64_t s = 0;
+  bounds[0] = 0;
+  for (int g = 0; g < G; ++g) {
+    uint64_t cur = 0;
+    while (s < S && cur + w[s] <= lo) { cur += w[s]; ++s; }
+    bounds[g + 1] = s;
+  }
+  bounds[G] = S;
+}
+
+void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, double tol,
+                    uint64_t seed, const double* const* init, const AlsOut& out,
+                    splatt_stats* st) {
+  cudaStream_t s = ctx->stream;
+  const int N = X.N;
+  const int ld = padded_ld(R);
+  const int G = ctx->comm ? ctx->comm->nranks : 1;
+  const int me = ctx->comm ? ctx->comm->rank : 0;
+  EventTimer tm;
+  tm.s = s;
+  tm.on = (st != nullptr);
+  uint64_t launches0 = ctx->kernel_launches;
+
+  // ---------------------------------------------------------------- validate
+  tm.begin(kBuild);
+  if (!validate_coo_device(ctx, X.ind, X.nnz, N, X.dims))
+    fail(SPLATT_ERR_BADINPUT, "index out of range for its mode");
+  DevBuf<double> normx(1, s);
+  norm_sq(ctx, X.vals, X.nnz, normx.p);
+  double h_normx = 0.0;
+  SB_CUDA(cudaMemcpyAsync(&h_normx, normx.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+  SB_CUDA(cudaStreamSynchronize(s));
+  if (!(h_normx > 0.0)) fail(SPLATT_ERR_EMPTY, "||X|| = 0");
+
+  // ------------------------------------------- partition + CSF build per mode
+  std::vector<std::vector<uint64_t>> bounds(N);
+  std::vector<std::unique_ptr<DevCsf>> csf(N);
+  for (int n = 0; n < N; ++n) {
+    csf[n] = std::make_unique<DevCsf>();
+    if (G == 1) {
+      bounds[n] = {0, X.dims[n]};
+      build_csf(ctx, X.ind, X.vals, X.nnz, N, X.dims, n, *csf[n]);
+      continue;
+    }
+    DevBuf<unsigned long long> cnt(X.dims[n], s);
+    SB_CUDA(cudaMemsetAsync(cnt.p, 0, X.dims[n] * 8, s));
+    histogram_kernel<<<blocks_for(ctx, X.nnz), 256, 0, s>>>(X.ind[n], X.nnz, cnt.p);
+    SB_CHECK_LAUNCH(ctx);
+    std::vector<uint64_t> hc(X.dims[n]);
+    SB_CUDA(cudaMemcpyAsync(hc.data(), cnt.p, X.dims[n] * 8, cudaMemcpyDeviceToHost, s));
+    SB_CUDA(cudaStreamSynchronize(s));
+    bounds[n].assign(G + 1, 0);
+    host_partition(hc.data(), X.dims[n], G, bounds[n].data());
+    const uint32_t lo = (uint32_t)bounds[n][me], hi = (uint32_t)bounds[n][me + 1];
+    DevBuf<uint32_t> flag(X.nnz, s), pos(X.nnz, s);
+    owned_flags_kernel<<<blocks_for(ctx, X.nnz), 256, 0, s>>>(X.ind[n], X.nnz, lo, hi, flag.p);
+    SB_CHECK_LAUNCH(ctx);
+    size_t tb = 0;
+    SB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag.p, pos.p, (int)X.nnz, s));
+    DevBuf<uint8_t> temp(tb, s);
+    SB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, flag.p, pos.p, (int)X.nnz, s));
+    uint64_t local = 0;
+    for (uint64_t i = lo; i < hi; ++i) local += hc[i];
+    if (local == 0) {  // a rank with no nonzeros of this mode: empty CSF
+      csf[n]->N = N;
+      csf[n]->nnz = 0;
+      continue;
+    }
+    DevBuf<uint32_t> lind[SPLATT_MAX_NMODES];
+    DevBuf<double> lval(local, s);
+    Compact c{};
+    c.N = N;
+    for (int m = 0; m < N; ++m) {
+      lind[m].alloc(local, s);
+      c.src[m] = X.ind[m];
+      c.dst[m] = lind[m].p;
+    }
+    compact_kernel<<<blocks_for(ctx, X.nnz), 256, 0, s>>>(c, X.vals, lval.p, flag.p, pos.p, X.nnz);
+    SB_CHECK_LAUNCH(ctx);
+    const uint32_t* lp[SPLATT_MAX_NMODES];
+    for (int m = 0; m < N; ++m) lp[m] = lind[m].p;
+    build_csf(ctx, lp, lval.p, local, N, X.dims, n, *csf[n]);
+  }
+  tm.end();
+
+  // -------------------------------------------------------------- factors
+  std::vector<DevBuf<double>> A(N);
+  uint64_t maxI = 0, base = 0;
+  for (int n = 0; n < N; ++n) {
+    A[n].alloc(X.dims[n] * ld, s);
+    maxI = std::max(maxI, X.dims[n]);
+    if (init) {
+      SB_CUDA(cudaMemsetAsync(A[n].p, 0, X.dims[n] * ld * sizeof(double), s));
+      SB_CUDA(cudaMemcpy2DAsync(A[n].p, ld * sizeof(double), init[n], R * sizeof(double),
+                                R * sizeof(double), X.dims[n], cudaMemcpyDefault, s));
+    } else {
+      init_factor(ctx, A[n].p, X.dims[n], R, ld, seed, base);   // C-2
+    }
+    base += X.dims[n] * (uint64_t)R;
+  }
+  const double* fac[SPLATT_MAX_NMODES] = {nullptr};
+  for (int n = 0; n < N; ++n) fac[n] = A[n].p;
+  const size_t RR = (size_t)R * R;
+  DevBuf<double> Gall(N * RR, s), stats(stats_len(R), s), L(RR, s), lambda(R, s), inner(1, s),
+      M(maxI * ld, s), fit_hist(max_iters, s), nu(R, s);
+  DevBuf<int> status(1, s);
+  SB_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int), s));
+  SB_CUDA(cudaMemsetAsync(fit_hist.p, 0, max_iters * sizeof(double), s));
+  tm.begin(kAta);
+  for (int n = 0; n < N; ++n) {   // initial Grams (C-4); factors are replicated
+    rows_solve_stats(ctx, nullptr, A[n].p, 0, X.dims[n], R, ld, nullptr, false, false, nullptr,
+                     stats.p);
+    gram_from_stats(ctx, stats.p, R, Gall.p + n * RR);
+  }
+  tm.end();
+
+  // ----------------------------------------------------------------- loop
+  double mttkrp_bytes = 0.0;
+  uint64_t mttkrp_launches = 0;
+  std::vector<double> h_hist(max_iters, 0.0);
+  int it_done = 0;
+  cudaEvent_t loop_a = nullptr, loop_b = nullptr;
+  SB_CUDA(cudaEventCreate(&loop_a));
+  SB_CUDA(cudaEventCreate(&loop_b));
+  SB_CUDA(cudaEventRecord(loop_a, s));
+  for (int it = 1; it <= max_iters; ++it) {
+    for (int n = 0; n < N; ++n) {
+      const uint64_t lo = bounds[n][me], hi = bounds[n][me + 1];
+      tm.begin(kInverse);
+      hadamard_cholesky(ctx, Gall.p, N, n, R, L.p, status.p);           // lines 4/7/10 + potrf
+      tm.end();
+      if (csf[n]->nnz) {
+        mttkrp_root(ctx, *csf[n], fac, M.p, X.dims[n], ld, R, &tm, kMttkrp);  // lines 5/8/11
+        mttkrp_bytes += mttkrp_alg_bytes(*csf[n], R);
+        ++mttkrp_launches;
+      } else {
+        SB_CUDA(cudaMemsetAsync(M.p, 0, X.dims[n] * ld * sizeof(double), s));
+      }
+      tm.begin(kInverse);
+      rows_solve_stats(ctx, M.p, A[n].p, lo, hi, R, ld, L.p, true, n == N - 1, status.p,
+                       stats.p);                                           // potrs + stats
+      tm.end();
+      if (G > 1) {
+        tm.begin(kComm);
+        ctx->comm->allreduce_sum(stats.p, stats_sum_len(R), s);
+        ctx->comm->allreduce_max(stats.p + stats_max_off(R), R, s);
+        ctx->comm->allgatherv_rows(A[n].p, bounds[n], ld, s);
+        tm.end();
+      }
+      tm.begin(kNorm);
+      lambda_gram(ctx, stats.p, R, it == 1, lambda.p, Gall.p + n * RR, inner.p);  // line 6
+      scale_columns(ctx, A[n].p, 0, X.dims[n], R, ld, lambda.p);
+      tm.end();
+    }
+    tm.begin(kFit);
+    fit(ctx, Gall.p, N, R, lambda.p, inner.p, normx.p, fit_hist.p + (it - 1));   // line 13
+    tm.end();
+    it_done = it;
+    if (tol > 0.0 && it >= 2) {
+      double two[2];
+      SB_CUDA(cudaMemcpyAsync(two, fit_hist.p + (it - 2), 2 * sizeof(double),
+                              cudaMemcpyDeviceToHost, s));
+      SB_CUDA(cudaStreamSynchronize(s));
+      if (std::fabs(two[1] - two[0]) < tol) break;                        // C-11
+    }
+  }
+  SB_CUDA(cudaEventRecord(loop_b, s));
+  int h_status = 0;
+  SB_CUDA(cudaMemcpyAsync(&h_status, status.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SB_CUDA(cudaMemcpyAsync(h_hist.data(), fit_hist.p, max_iters * sizeof(double),
+                          cudaMemcpyDeviceToHost, s));
+  SB_CUDA(cudaStreamSynchronize(s));
+  float loop_ms = 0.f;
+  cudaEventElapsedTime(&loop_ms, loop_a, loop_b);
+  cudaEventDestroy(loop_a);
+  cudaEventDestroy(loop_b);
+  if (h_status) fail(SPLATT_ERR_SINGULAR, "Gram Hadamard product is singular (after ridge)");
+
+  // ------------------------------------------------------------- finalise (C-12)
+  for (int n = 0; n < N; ++n) {
+    fold_norms(ctx, Gall.p + n * RR, R, lambda.p, nu.p);
+    scale_columns(ctx, A[n].p, 0, X.dims[n], R, ld, nu.p);
+    SB_CUDA(cudaMemcpy2DAsync(out.factors[n], R * sizeof(double), A[n].p, ld * sizeof(double),
+                              R * sizeof(double), X.dims[n], cudaMemcpyDefault, s));
+  }
+  SB_CUDA(cudaMemcpyAsync(out.lambda, lambda.p, R * sizeof(double), cudaMemcpyDefault, s));
+  SB_CUDA(cudaStreamSynchronize(s));
+  *out.fit = h_hist[it_done - 1];
+  *out.iters = it_done;
+  if (out.fit_history)
+    for (int i = 0; i < it_done; ++i) out.fit_history[i] = h_hist[i];
+
+  if (st) {
+    double t[kNumCat] = {0};
+    tm.collect(t, kNumCat);
+    st->t_mttkrp = t[kMttkrp];
+    st->t_build = t[kBuild];
+    st->t_ata = t[kAta];
+    st->t_norm = t[kNorm];
+    st->t_fit = t[kFit];
+    st->t_inverse = t[kInverse];
+    st->t_comm = t[kComm];
+    st->t_loop = loop_ms * 1e-3;
+    st->mttkrp_alg_bytes = mttkrp_bytes;
+    st->mttkrp_launches = mttkrp_launches;
+    st->kernel_launches = ctx->kernel_launches - launches0;
+    for (int n = 0; n < N; ++n)
+      for (int l = 0; l < N; ++l) st->csf_nodes[n][l] = csf[n]->nodes[l];
+    st->iters = it_done;
+    st->nranks = G;
+  }
+}
+
+}  // namespace sb

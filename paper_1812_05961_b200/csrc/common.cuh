@@ -1,0 +1,43 @@
+// common.cuh — shared internals of libsplatt_b200 (CUDA path only; no oracle code).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/splatt_b200.h"
+
+namespace sb {
+
+// Internal failure carrying an ABI status; caught at the C boundary (abi.cu).
+struct Error : std::runtime_error {
+  splatt_status code;
+  Error(splatt_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(splatt_status c, const std::string& m) { throw Error(c, m); }
+
+#define SB_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      ::sb::fail(e_ == cudaErrorMemoryAllocation ? SPLATT_ERR_NOMEM : SPLATT_ERR_CUDA,  \
+                 std::string(#call) + ": " + cudaGetErrorString(e_));                   \
+  } while (0)
+
+#define SB_CHECK_LAUNCH(ctx) \
+  do { (ctx)->kernel_launches++; SB_CUDA(cudaGetLastError()); } while (0)
+
+#define SB_REQUIRE(cond, msg) \
+  do { if (!(cond)) ::sb::fail(SPLATT_ERR_BADINPUT, msg); } while (0)
+
+// Internal leading dimension of every factor / MTTKRP buffer: ceil(R/4)*4 doubles,
+// so each row is a whole number of 32-byte sectors and 256-bit loads stay aligned
+// (SURVEY.md §8(a) a3).
+inline int padded_ld(int R) { return (R + 3) / 4 * 4; }
+
+inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+}  // namespace sb

@@ -1,0 +1,302 @@
+// csf.cu — device COO -> CSF builder.
+//
+// For CSF_n with level order perm (root n first): the nonzeros are put in the
+// lexicographic order of (ind[perm[0]], ..., ind[perm[N-1]]), ties by input position
+// (stable), using LSD radix sorts of packed composite keys (one 64-bit pass group when
+// the coordinate bits fit, else several stable groups, least significant first).
+// Level-l nodes are the maximal runs of equal (perm[0..l]) prefixes: a start flag per
+// position, an inclusive scan numbering the nodes, and a scatter of ids/ptr.  All
+// integer work, so the result is bit-exact against any correct implementation.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <numeric>
+
+#include "csf.hpp"
+
+namespace sb {
+
+namespace {
+
+struct IndSet {
+  const uint32_t* p[SPLATT_MAX_NMODES];
+  uint64_t dims[SPLATT_MAX_NMODES];
+  int N;
+};
+
+__global__ void validate_kernel(IndSet s, uint64_t nnz, int* bad) {
+  int local = 0;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    for (int m = 0; m < s.N; ++m) local |= (s.p[m][j] >= s.dims[m]);
+  }
+  if (__any_sync(0xffffffffu, local) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+}
+
+// Composite key of levels [lo, hi) (level order), most significant = lo.
+struct KeySpec {
+  const uint32_t* src[SPLATT_MAX_NMODES];  // per level (already in level order)
+  int shift[SPLATT_MAX_NMODES];
+  int lo, hi;
+};
+
+__global__ void pack_keys_kernel(KeySpec ks, uint64_t nnz, const uint32_t* __restrict__ order,
+                                 uint64_t* __restrict__ keys, uint32_t* __restrict__ pos) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t q = order ? order[j] : (uint32_t)j;
+    uint64_t k = 0;
+    for (int l = ks.lo; l < ks.hi; ++l) k |= (uint64_t)ks.src[l][q] << ks.shift[l];
+    keys[j] = k;
+    if (!order) pos[j] = (uint32_t)j;
+  }
+}
+
+struct CoordOut {
+  const uint32_t* src[SPLATT_MAX_NMODES];
+  uint32_t* dst[SPLATT_MAX_NMODES];
+  int N;
+};
+
+__global__ void gather_kernel(CoordOut co, uint64_t nnz, const uint32_t* __restrict__ P,
+                              const double* __restrict__ vin, double* __restrict__ vout) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t q = P[j];
+    for (int l = 0; l < co.N; ++l) co.dst[l][j] = co.src[l][q];
+    vout[j] = vin[q];
+  }
+}
+
+// node[l][j] = 1 iff a level-l node starts at sorted position j (prefix 0..l changed).
+struct FlagOut {
+  const uint32_t* c[SPLATT_MAX_NMODES];
+  uint32_t* node[SPLATT_MAX_NMODES];
+  int N;
+};
+
+__global__ void level_flags_kernel(FlagOut f, uint64_t nnz) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    int d = f.N;  // first level whose coordinate differs from position j-1
+    if (j == 0) {
+      d = 0;
+    } else {
+      for (int l = f.N - 1; l >= 0; --l)
+        if (f.c[l][j] != f.c[l][j - 1]) d = l;
+    }
+    for (int l = 0; l < f.N - 1; ++l) f.node[l][j] = (d <= l) ? 1u : 0u;
+  }
+}
+
+// After the inclusive scans node[l][j] = 1 + index of the level-l node containing j.
+__global__ void scatter_level_kernel(uint64_t nnz, const uint32_t* __restrict__ node_l,
+                                     const uint32_t* __restrict__ node_child,  // null: leaves
+                                     const uint32_t* __restrict__ c_l, uint32_t* __restrict__ ids,
+                                     uint32_t* __restrict__ ptr, uint64_t n_nodes,
+                                     uint64_t n_children) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = node_l[j];
+    const bool start = (j == 0) || (node_l[j - 1] != k);
+    if (start) {
+      ids[k - 1] = c_l[j];
+      ptr[k - 1] = node_child ? node_child[j] - 1 : (uint32_t)j;
+    }
+    if (j == 0) ptr[n_nodes] = (uint32_t)n_children;
+  }
+}
+
+struct PtrSet {
+  const uint32_t* ptr[SPLATT_MAX_NMODES];
+  uint64_t nodes[SPLATT_MAX_NMODES];
+  int N;
+};
+
+// Largest i in [0, n) with ptr[i] <= x (ptr has n+1 non-decreasing entries, ptr[0] = 0).
+__device__ __forceinline__ uint32_t find_node(const uint32_t* __restrict__ ptr, uint64_t n,
+                                              uint32_t x) {
+  uint64_t lo = 0, hi = n;  // answer in [lo, hi)
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (ptr[mid] <= x) lo = mid; else hi = mid;
+  }
+  return (uint32_t)lo;
+}
+
+__global__ void chunk_table_kernel(PtrSet ps, uint64_t nnz, int chunk, uint64_t nchunks,
+                                   uint32_t* __restrict__ tab) {
+  const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  const int N = ps.N;
+  const uint32_t k0 = (uint32_t)(c * (uint64_t)chunk);
+  uint32_t b[SPLATT_MAX_NMODES];
+  b[N - 2] = find_node(ps.ptr[N - 2], ps.nodes[N - 2], k0);
+  bool starts = ps.ptr[N - 2][b[N - 2]] == k0;
+  for (int l = N - 3; l >= 0; --l) {
+    b[l] = find_node(ps.ptr[l], ps.nodes[l], b[l + 1]);
+    starts = starts && (ps.ptr[l][b[l]] == b[l + 1]);
+  }
+  for (int l = 0; l <= N - 2; ++l) tab[c * N + l] = b[l];
+  tab[c * N + N - 1] = starts ? 0u : 1u;
+}
+
+inline int grid_for(splatt_ctx* ctx, uint64_t n, int block = 256) {
+  const uint64_t want = ceil_div(n, block);
+  const uint64_t cap = (uint64_t)ctx->num_sms * 16;
+  return (int)std::max<uint64_t>(1, std::min(want, cap));
+}
+
+int bits_for(uint64_t dim) {
+  if (dim <= 1) return 0;
+  int b = 0;
+  uint64_t v = dim - 1;
+  while (v) { ++b; v >>= 1; }
+  return b;
+}
+
+}  // namespace
+
+void csf_perm(int N, const uint64_t* dims, int root, int* perm) {
+  std::vector<int> rest;
+  for (int m = 0; m < N; ++m)
+    if (m != root) rest.push_back(m);
+  std::stable_sort(rest.begin(), rest.end(), [&](int a, int b) { return dims[a] < dims[b]; });
+  perm[0] = root;
+  for (int k = 0; k < N - 1; ++k) perm[k + 1] = rest[k];
+}
+
+bool validate_coo_device(splatt_ctx* ctx, const uint32_t* const* d_ind, uint64_t nnz, int N,
+                         const uint64_t* dims) {
+  IndSet s{};
+  for (int m = 0; m < N; ++m) { s.p[m] = d_ind[m]; s.dims[m] = dims[m]; }
+  s.N = N;
+  DevBuf<int> bad(1, ctx->stream);
+  SB_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
+  validate_kernel<<<grid_for(ctx, nnz), 256, 0, ctx->stream>>>(s, nnz, bad.p);
+  SB_CHECK_LAUNCH(ctx);
+  int h = 0;
+  SB_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  SB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return h == 0;
+}
+
+void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_vals, uint64_t nnz,
+               int N, const uint64_t* dims, int root, DevCsf& out) {
+  cudaStream_t st = ctx->stream;
+  if (nnz >= (1ull << 31)) fail(SPLATT_ERR_UNSUPPORTED, "nnz >= 2^31 not supported");
+  out.N = N;
+  out.nnz = nnz;
+  csf_perm(N, dims, root, out.perm);
+  int bits[SPLATT_MAX_NMODES];
+  const uint32_t* lvl_src[SPLATT_MAX_NMODES];
+  for (int l = 0; l < N; ++l) {
+    bits[l] = bits_for(dims[out.perm[l]]);
+    lvl_src[l] = d_ind[out.perm[l]];
+  }
+  // Key groups, least significant first: levels [lo, hi) with <= 64 bits in total.
+  std::vector<std::pair<int, int>> groups;
+  {
+    int hi = N, acc = 0;
+    for (int l = N - 1; l >= 0; --l) {
+      if (acc + bits[l] > 64) { groups.push_back({l + 1, hi}); hi = l + 1; acc = 0; }
+      acc += bits[l];
+    }
+    groups.push_back({0, hi});
+  }
+  const int grid = grid_for(ctx, nnz);
+  DevBuf<uint64_t> kA(nnz, st), kB(nnz, st);
+  DevBuf<uint32_t> pA(nnz, st), pB(nnz, st);
+  DevBuf<uint8_t> temp;
+  size_t temp_bytes = 0;
+  SB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, kA.p, kB.p, pA.p, pB.p, (int)nnz, 0,
+                                          64, st));
+  temp.alloc(temp_bytes, st);
+  uint32_t* order = nullptr;  // current permutation (sorted position -> input position)
+  for (size_t g = 0; g < groups.size(); ++g) {
+    KeySpec ks{};
+    ks.lo = groups[g].first;
+    ks.hi = groups[g].second;
+    int sh = 0, total = 0;
+    for (int l = ks.hi - 1; l >= ks.lo; --l) { ks.src[l] = lvl_src[l]; ks.shift[l] = sh; sh += bits[l]; }
+    total = sh;
+    // order == nullptr: first group, positions are the identity (written into pA).
+    pack_keys_kernel<<<grid, 256, 0, st>>>(ks, nnz, order, kA.p, pA.p);
+    SB_CHECK_LAUNCH(ctx);
+    uint32_t* pin = order ? order : pA.p;
+    uint32_t* pout = (pin == pB.p) ? pA.p : pB.p;
+    if (total > 0) {
+      SB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, kA.p, kB.p, pin, pout, (int)nnz, 0,
+                                              total, st));
+    } else {
+      SB_CUDA(cudaMemcpyAsync(pout, pin, nnz * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    order = pout;
+  }
+  kA.release();
+  kB.release();
+  temp.release();
+
+  // Sorted coordinates per level and the permuted values.
+  DevBuf<uint32_t> coord[SPLATT_MAX_NMODES];
+  CoordOut co{};
+  co.N = N;
+  for (int l = 0; l < N; ++l) {
+    coord[l].alloc(nnz, st);
+    co.src[l] = lvl_src[l];
+    co.dst[l] = coord[l].p;
+  }
+  out.vals.alloc(nnz, st);
+  gather_kernel<<<grid, 256, 0, st>>>(co, nnz, order, d_vals, out.vals.p);
+  SB_CHECK_LAUNCH(ctx);
+  pA.release();
+  pB.release();
+
+  // Node numbering per internal level.
+  DevBuf<uint32_t> node[SPLATT_MAX_NMODES];
+  FlagOut fo{};
+  fo.N = N;
+  for (int l = 0; l < N; ++l) fo.c[l] = coord[l].p;
+  for (int l = 0; l < N - 1; ++l) { node[l].alloc(nnz, st); fo.node[l] = node[l].p; }
+  level_flags_kernel<<<grid, 256, 0, st>>>(fo, nnz);
+  SB_CHECK_LAUNCH(ctx);
+  temp_bytes = 0;
+  SB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, node[0].p, node[0].p, (int)nnz, st));
+  temp.alloc(temp_bytes, st);
+  for (int l = 0; l < N - 1; ++l)
+    SB_CUDA(cub::DeviceScan::InclusiveSum(temp.p, temp_bytes, node[l].p, node[l].p, (int)nnz, st));
+  temp.release();
+  std::vector<uint32_t> counts(N, 0);
+  for (int l = 0; l < N - 1; ++l)
+    SB_CUDA(cudaMemcpyAsync(&counts[l], node[l].p + (nnz - 1), 4, cudaMemcpyDeviceToHost, st));
+  SB_CUDA(cudaStreamSynchronize(st));
+  for (int l = 0; l < N - 1; ++l) out.nodes[l] = counts[l];
+  out.nodes[N - 1] = nnz;
+  for (int l = 0; l < N - 1; ++l) {
+    out.ids[l].alloc(out.nodes[l], st);
+    out.ptr[l].alloc(out.nodes[l] + 1, st);
+    const uint32_t* child = (l == N - 2) ? nullptr : node[l + 1].p;
+    scatter_level_kernel<<<grid, 256, 0, st>>>(nnz, node[l].p, child, coord[l].p, out.ids[l].p,
+                                               out.ptr[l].p, out.nodes[l], out.nodes[l + 1]);
+    SB_CHECK_LAUNCH(ctx);
+  }
+  out.ids[N - 1] = std::move(coord[N - 1]);
+  out.tab_chunk = 0;
+  out.nchunks = 0;
+  out.tab.release();
+}
+
+void ensure_chunk_table(splatt_ctx* ctx, DevCsf& c, int chunk) {
+  if (c.tab_chunk == chunk && c.tab.p) return;
+  c.nchunks = ceil_div(c.nnz, chunk);
+  c.tab.alloc(c.nchunks * c.N, ctx->stream);
+  PtrSet ps{};
+  ps.N = c.N;
+  for (int l = 0; l < c.N - 1; ++l) { ps.ptr[l] = c.ptr[l].p; ps.nodes[l] = c.nodes[l]; }
+  chunk_table_kernel<<<(unsigned)ceil_div(c.nchunks, 256), 256, 0, ctx->stream>>>(
+      ps, c.nnz, chunk, c.nchunks, c.tab.p);
+  SB_CHECK_LAUNCH(ctx);
+  c.tab_chunk = chunk;
+}
+
+}  // namespace sb

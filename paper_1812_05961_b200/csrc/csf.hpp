@@ -1,0 +1,52 @@
+// csf.hpp — device-resident compressed sparse fiber tensors.
+#pragma once
+#include <memory>
+
+#include "ctx.hpp"
+
+namespace sb {
+
+// One CSF tree.  Level l < N-1: ids[l] (nodes[l]) and ptr[l] (nodes[l]+1, offsets into
+// level l+1); leaf level N-1: ids[N-1] (nnz) and vals (nnz).  perm[l] = mode at level l.
+struct DevCsf {
+  int N = 0;
+  uint64_t nnz = 0;
+  int perm[SPLATT_MAX_NMODES] = {0};
+  uint64_t nodes[SPLATT_MAX_NMODES] = {0};
+  DevBuf<uint32_t> ids[SPLATT_MAX_NMODES];
+  DevBuf<uint32_t> ptr[SPLATT_MAX_NMODES];
+  DevBuf<double> vals;
+  // MTTKRP work table (built on first use for a chunk size): per chunk of `tab_chunk`
+  // leaves, the node index at every internal level containing the chunk's first leaf
+  // plus a flag word (bit 0: the root slice started before the chunk).
+  int tab_chunk = 0;
+  uint64_t nchunks = 0;
+  DevBuf<uint32_t> tab;
+};
+
+// perm: root first, then the other modes by ascending length, ties to the lower id
+// (SPEC.md:131).
+void csf_perm(int N, const uint64_t* dims, int root, int* perm);
+
+// Build CSF rooted at `root` from a device COO (ind[m], vals; nnz entries).
+void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_vals, uint64_t nnz,
+               int N, const uint64_t* dims, int root, DevCsf& out);
+
+// Ensure the chunk table for `chunk` leaves per work unit exists.
+void ensure_chunk_table(splatt_ctx* ctx, DevCsf& c, int chunk);
+
+// Device validation: returns true iff every ind[m][p] < dims[m]  (synchronises).
+bool validate_coo_device(splatt_ctx* ctx, const uint32_t* const* d_ind, uint64_t nnz, int N,
+                         const uint64_t* dims);
+
+}  // namespace sb
+
+struct splatt_csf {
+  int N = 0;
+  uint64_t dims[SPLATT_MAX_NMODES] = {0};
+  int policy = SPLATT_CSF_ALL;
+  int ncsf = 0;
+  std::unique_ptr<sb::DevCsf> csf[SPLATT_MAX_NMODES];
+  int mode_csf[SPLATT_MAX_NMODES] = {0};
+  splatt_ctx* ctx = nullptr;
+};

@@ -1,0 +1,55 @@
+// dense.hpp — the small fp64 steps around MTTKRP.
+#pragma once
+#include "ctx.hpp"
+
+namespace sb {
+
+// Layout of the per-mode statistics vector (all doubles), reduced over rows (and over
+// ranks with comm): [0, R*R) Gram of the unnormalised rows (symmetric), [R*R] inner
+// product sum M .* A, [R*R+1, R*R+1+R) column max |a|.  The first R*R+1 entries are
+// sums, the last R maxima, so one all-reduce of each kind combines ranks.
+inline size_t stats_len(int R) { return (size_t)R * R + R + 1; }
+inline size_t stats_sum_len(int R) { return (size_t)R * R + 1; }
+inline size_t stats_max_off(int R) { return (size_t)R * R + 1; }
+
+// a3: A[i, r] = u(seed, base + i*R + r) for r < R (counter-based splitmix64), pads 0.
+void init_factor(splatt_ctx* ctx, double* A, uint64_t I, int R, int ld, uint64_t seed,
+                 uint64_t base);
+
+// sum of squares of vals (deterministic two-pass reduction) into d_out[0].
+void norm_sq(splatt_ctx* ctx, const double* vals, uint64_t nnz, double* d_out);
+
+// a5 + a7 (factor): V = *_{m != n} G_m (ascending m), Cholesky V = L L^T with the
+// 1e-12*max diag pivot test and one 1e-12*trace/R ridge retry.  G_all: N x R*R.
+// L: R*R (lower, row-major).  status: set to 1 on failure (never cleared here).
+void hadamard_cholesky(splatt_ctx* ctx, const double* G_all, int N, int n, int R, double* L,
+                       int* status);
+
+// a7 (solve) + a9/a8/a10 partials: for rows [lo, hi): if solve, A[i,:] = M[i,:] V^-1
+// (forward/back substitution with L); then accumulate the Gram of the rows, the
+// column max |A| and (if inner) sum M .* A.  Reduced to stats (stats_len(R)).
+// If !solve, M is ignored and A is only read.  Skipped when *status != 0.
+void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, uint64_t hi,
+                      int R, int ld, const double* L, bool solve, bool inner, const int* status,
+                      double* stats);
+
+// a8 + a9: lambda (first: 2-norm = sqrt(G~_rr); else max(1, colmax)), G_n =
+// G~ / (lambda lambda^T) (mirrored), inner_out = stats inner.
+void lambda_gram(splatt_ctx* ctx, const double* stats, int R, bool first, double* lambda,
+                 double* G_n, double* inner_out);
+
+// Mirror the upper Gram of stats into G (R x R) — initial Grams.
+void gram_from_stats(splatt_ctx* ctx, const double* stats, int R, double* G);
+
+// A[i, r] /= lambda[r] for lambda[r] > 0, rows [lo, hi).
+void scale_columns(splatt_ctx* ctx, double* A, uint64_t lo, uint64_t hi, int R, int ld,
+                   const double* lambda);
+
+// a10: fit = 1 - sqrt(max(0, nx + zz - 2 inner)) / sqrt(nx), zz = lambda^T (*_m G_m) lambda.
+void fit(splatt_ctx* ctx, const double* G_all, int N, int R, const double* lambda,
+         const double* inner, const double* normx_sq, double* fit_out);
+
+// a11 (finalise one mode): nu_r = sqrt(G_n[r,r]); lambda_r *= nu_r; nu written to nu.
+void fold_norms(splatt_ctx* ctx, const double* G_n, int R, double* lambda, double* nu);
+
+}  // namespace sb

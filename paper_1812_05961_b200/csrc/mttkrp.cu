@@ -1,0 +1,355 @@
+// mttkrp.cu — root-mode CSF MTTKRP for sm_100a (PAPER.md:182-185,
+// Alg. 1 lines 5/8/11; "no-lock" root traversal PAPER.md:469).
+//
+//   M[i, :] = sum_{slices i} sum_{fibers} ( sum_{leaves} v * A_leaf[k, :] ) (*) A_mid[j, :] ...
+//
+// Design:
+//  * Work unit = a fixed chunk of CH consecutive leaves of the CSF, handled by a lane
+//    group of G lanes (G = next pow2 of ld/4; each lane owns 4 consecutive columns
+//    and moves them with one 256-bit load).  Fixed-size leaf chunks balance the
+//    power-law slices (a 13.8M-nonzero slice is just many chunks) — SURVEY.md §8(a')1a.
+//  * A group walks its chunk in batches of 32 leaves.  Per batch it loads windows of
+//    leaf ids/values (streamed, L1 no-allocate) and of every internal level's ptr,
+//    turns them into 32-bit "node closes here" masks (segment flags derived from ptr,
+//    §8(a')2), and then runs the leaves sequentially with register accumulators per
+//    level: leaf rows are FMA'd into the fiber accumulator, a closing node multiplies
+//    its accumulator by its own factor row and pushes it one level up, and a closing
+//    slice writes its output row.
+//  * Rows in flight: the U leaf rows (and the rows of the nodes they close) of a
+//    sub-batch are all issued before any is consumed (Little's law, §8(a')4).
+//  * Slices wholly inside a chunk are written with plain 256-bit stores (conflict-
+//    free: rows are owned); the <= 2 slices per chunk that cross a chunk boundary are
+//    accumulated with fp64 atomics into the zero-filled output.
+#include <algorithm>
+
+#include "csf.hpp"
+#include "mttkrp.hpp"
+
+namespace sb {
+
+namespace {
+
+template <int N>
+struct Args {
+  const uint32_t* ids[N];
+  const uint32_t* ptr[N];     // levels 0..N-2
+  const double* fac[N];       // fac[l] = factor of mode perm[l] (l >= 1)
+  uint32_t nodes[N];
+  const double* vals;
+  double* out;
+  const uint32_t* tab;
+  uint32_t nnz, nchunks, chunk;
+  int ld, R;
+};
+
+struct d4 { double x, y, z, w; };
+
+__device__ __forceinline__ d4 ldg_row(const double* p) {
+  d4 r;
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_stream_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_row(double* p, const d4& v) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z),
+               "d"(v.w) : "memory");
+}
+__device__ __forceinline__ void atomic_row(double* p, const d4& v) {
+  atomicAdd(p + 0, v.x);
+  atomicAdd(p + 1, v.y);
+  atomicAdd(p + 2, v.z);
+  atomicAdd(p + 3, v.w);
+}
+// Columns >= R of the output are written 0 whatever the factors' pad columns hold
+// (every column is computed independently, so pads never touch real columns).
+__device__ __forceinline__ d4 mask_pad(d4 v, int col, int R) {
+  if (col + 0 >= R) v.x = 0.0;
+  if (col + 1 >= R) v.y = 0.0;
+  if (col + 2 >= R) v.z = 0.0;
+  if (col + 3 >= R) v.w = 0.0;
+  return v;
+}
+__device__ __forceinline__ uint32_t lowmask(uint32_t n) {
+  return n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
+}
+template <int G>
+__device__ __forceinline__ uint32_t group_or(uint32_t m, unsigned gmask) {
+#pragma unroll
+  for (int o = G / 2; o >= 1; o >>= 1) m |= __shfl_xor_sync(gmask, m, o, G);
+  return m;
+}
+__device__ __forceinline__ void fma4(d4& acc, double v, const d4& r) {
+  acc.x = fma(v, r.x, acc.x);
+  acc.y = fma(v, r.y, acc.y);
+  acc.z = fma(v, r.z, acc.z);
+  acc.w = fma(v, r.w, acc.w);
+}
+__device__ __forceinline__ void fma4v(d4& acc, const d4& a, const d4& r) {
+  acc.x = fma(a.x, r.x, acc.x);
+  acc.y = fma(a.y, r.y, acc.y);
+  acc.z = fma(a.z, r.z, acc.z);
+  acc.w = fma(a.w, r.w, acc.w);
+}
+
+// NM = N-2 internal levels below the root that carry factor rows (>= 1 for N >= 3).
+template <int N, int G, int U>
+__global__ void __launch_bounds__(256) mttkrp_root_kernel(const Args<N> a) {
+  constexpr int E = 32 / G;  // window entries per lane
+  constexpr int NM = N - 2;
+  const int lane = threadIdx.x & 31;
+  const int q = lane & (G - 1);
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  const uint32_t group = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const uint32_t ngroups = gridDim.x * blockDim.x / G;
+  const bool active = 4 * q < a.ld;
+  const int col = 4 * q;
+
+  for (uint32_t c = group; c < a.nchunks; c += ngroups) {
+    const uint32_t k0 = c * a.chunk;
+    const uint32_t k1 = min(k0 + a.chunk, a.nnz);
+    uint32_t base[N - 1];
+#pragma unroll
+    for (int l = 0; l < N - 1; ++l) base[l] = a.tab[(size_t)c * N + l];
+    const bool first_partial = a.tab[(size_t)c * N + N - 1] & 1u;
+    const uint32_t slice0 = base[0];
+    d4 acc[N - 1];
+#pragma unroll
+    for (int l = 0; l < N - 1; ++l) acc[l] = d4{0, 0, 0, 0};
+    int last_dep = N - 1;
+
+    for (uint32_t kb = k0; kb < k1; kb += 32) {
+      const uint32_t nb = min(32u, k1 - kb);
+      uint32_t lid[E];
+      double lv[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint32_t t = q + e * G;
+        lid[e] = 0;
+        lv[e] = 0.0;
+        if (t < nb) {
+          lid[e] = ld_stream_u32(a.ids[N - 1] + kb + t);
+          lv[e] = ld_stream_f64(a.vals + kb + t);
+        }
+      }
+      // Close masks.  msk[N-2]: bit t = leaf kb+t is the last child of its level-(N-2)
+      // node.  msk[l] (l < N-2): bit u = level-(l+1) node base[l+1]+u is a last child.
+      uint32_t msk[N - 1];
+      {
+        uint32_t m = 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint32_t idx = base[N - 2] + 1 + q + e * G;
+          if (idx <= a.nodes[N - 2]) {
+            const uint32_t pos = a.ptr[N - 2][idx] - 1u - kb;
+            if (pos < nb) m |= 1u << pos;
+          }
+        }
+        msk[N - 2] = group_or<G>(m, gmask);
+      }
+#pragma unroll
+      for (int l = N - 3; l >= 0; --l) {
+        uint32_t m = 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint32_t idx = base[l] + 1 + q + e * G;
+          if (idx <= a.nodes[l]) {
+            const uint32_t pos = a.ptr[l][idx] - 1u - base[l + 1];
+            if (pos < 32u) m |= 1u << pos;
+          }
+        }
+        msk[l] = group_or<G>(m, gmask);
+      }
+      uint32_t cnt[N - 1];
+      cnt[N - 2] = __popc(msk[N - 2]);
+#pragma unroll
+      for (int l = N - 3; l >= 0; --l) cnt[l] = __popc(msk[l] & lowmask(cnt[l + 1]));
+
+#pragma unroll
+      for (int sb = 0; sb < 32; sb += U) {
+        if ((uint32_t)sb < nb) {
+          d4 row[U];
+          d4 mid[U][NM];
+          double v[U];
+          int dep[U];
+          uint32_t nodei[U][N - 1];
+          uint32_t rid[U];
+          // phase 1: closing chains and node ids
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int t = sb + u;
+            const uint32_t id = __shfl_sync(gmask, lid[t / G], t % G, G);
+            v[u] = __shfl_sync(gmask, lv[t / G], t % G, G);
+            dep[u] = N - 1;
+            rid[u] = id;
+            if ((uint32_t)t < nb && ((msk[N - 2] >> t) & 1u)) {
+              uint32_t li = __popc(msk[N - 2] & lowmask(t));
+              nodei[u][N - 2] = base[N - 2] + li;
+              dep[u] = N - 2;
+#pragma unroll
+              for (int l = N - 3; l >= 0; --l) {
+                if (dep[u] == l + 1 && ((msk[l] >> li) & 1u)) {
+                  li = __popc(msk[l] & lowmask(li));
+                  nodei[u][l] = base[l] + li;
+                  dep[u] = l;
+                }
+              }
+            }
+          }
+          // phase 2: ids of the closing nodes (factor row ids / output row)
+          uint32_t nid[U][NM];
+          uint32_t oid[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+#pragma unroll
+            for (int l = 1; l <= NM; ++l) nid[u][l - 1] = dep[u] <= l ? a.ids[l][nodei[u][l]] : 0u;
+            oid[u] = dep[u] == 0 ? a.ids[0][nodei[u][0]] : 0u;
+          }
+          // phase 3: issue every row load of the sub-batch before consuming any
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int t = sb + u;
+            row[u] = d4{0, 0, 0, 0};
+            if ((uint32_t)t < nb && active)
+              row[u] = ldg_row(a.fac[N - 1] + (size_t)rid[u] * a.ld + col);
+#pragma unroll
+            for (int l = 1; l <= NM; ++l) {
+              mid[u][l - 1] = d4{0, 0, 0, 0};
+              if (dep[u] <= l && active)
+                mid[u][l - 1] = ldg_row(a.fac[l] + (size_t)nid[u][l - 1] * a.ld + col);
+            }
+          }
+          // phase 4: accumulate, push closed nodes up, write closed slices
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int t = sb + u;
+            if ((uint32_t)t < nb) {
+              fma4(acc[N - 2], v[u], row[u]);
+              const int d = dep[u];
+#pragma unroll
+              for (int l = NM; l >= 1; --l) {
+                if (d <= l) {
+                  fma4v(acc[l - 1], acc[l], mid[u][l - 1]);
+                  acc[l] = d4{0, 0, 0, 0};
+                }
+              }
+              if (d == 0) {
+                if (active) {
+                  double* o = a.out + (size_t)oid[u] * a.ld + col;
+                  const d4 w = mask_pad(acc[0], col, a.R);
+                  if (first_partial && nodei[u][0] == slice0) atomic_row(o, w);
+                  else st_row(o, w);
+                }
+                acc[0] = d4{0, 0, 0, 0};
+              }
+              last_dep = d;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int l = 0; l < N - 1; ++l) base[l] += cnt[l];
+    }
+    // Chunk end: fold the still-open levels (< last_dep) into the open slice's row.
+    if (last_dep > 0) {
+#pragma unroll
+      for (int l = NM; l >= 1; --l) {
+        if (l < last_dep && active) {
+          const uint32_t nid = a.ids[l][base[l]];
+          const d4 r = ldg_row(a.fac[l] + (size_t)nid * a.ld + col);
+          fma4v(acc[l - 1], acc[l], r);
+        }
+      }
+      if (active) {
+        const uint32_t i = a.ids[0][base[0]];
+        atomic_row(a.out + (size_t)i * a.ld + col, mask_pad(acc[0], col, a.R));
+      }
+    }
+  }
+}
+
+template <int N, int G, int U>
+void launch_t(splatt_ctx* ctx, const DevCsf& c, const double* const* fac_by_mode, double* out,
+              int ld, int R, int chunk) {
+  Args<N> a{};
+  for (int l = 0; l < N; ++l) {
+    a.ids[l] = c.ids[l].p;
+    a.ptr[l] = (l < N - 1) ? c.ptr[l].p : nullptr;
+    a.fac[l] = fac_by_mode[c.perm[l]];
+    a.nodes[l] = (uint32_t)c.nodes[l];
+  }
+  a.vals = c.vals.p;
+  a.out = out;
+  a.tab = c.tab.p;
+  a.nnz = (uint32_t)c.nnz;
+  a.nchunks = (uint32_t)c.nchunks;
+  a.chunk = (uint32_t)chunk;
+  a.ld = ld;
+  a.R = R;
+  const uint64_t groups_per_block = 256 / G;
+  const uint64_t blocks = ceil_div(c.nchunks, groups_per_block);
+  mttkrp_root_kernel<N, G, U><<<(unsigned)std::max<uint64_t>(1, blocks), 256, 0, ctx->stream>>>(a);
+  SB_CHECK_LAUNCH(ctx);
+}
+
+template <int N>
+void launch_n(splatt_ctx* ctx, const DevCsf& c, const double* const* f, double* out, int ld,
+              int R, int chunk) {
+  const int slots = ld / 4;
+  constexpr int U = (N <= 4) ? 4 : 2;
+  if (slots <= 2) launch_t<N, 2, U>(ctx, c, f, out, ld, R, chunk);
+  else if (slots <= 4) launch_t<N, 4, U>(ctx, c, f, out, ld, R, chunk);
+  else if (slots <= 8) launch_t<N, 8, U>(ctx, c, f, out, ld, R, chunk);
+  else if (slots <= 16) launch_t<N, 16, U>(ctx, c, f, out, ld, R, chunk);
+  else launch_t<N, 32, U>(ctx, c, f, out, ld, R, chunk);
+}
+
+}  // namespace
+
+int mttkrp_chunk_leaves(int N, int ld) {
+  (void)N;
+  (void)ld;
+  return 512;
+}
+
+double mttkrp_alg_bytes(const DevCsf& c, int R) {
+  // B_alg = CSF index/value bytes + gathered factor-row bytes:
+  // 12 B per leaf (id + value), 8 B per internal node (id + ptr) except the root level
+  // (8 B per slice: id + ptr), plus 8 R bytes per gathered row (one per leaf and one
+  // per internal node below the root).
+  double nodes_below_root = 0.0;
+  for (int l = 1; l < c.N - 1; ++l) nodes_below_root += (double)c.nodes[l];
+  const double nnz = (double)c.nnz;
+  return 12.0 * nnz + 8.0 * nodes_below_root + 8.0 * (double)c.nodes[0] +
+         8.0 * R * (nnz + nodes_below_root);
+}
+
+void mttkrp_root(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, double* out,
+                 uint64_t out_rows, int ld, int R, EventTimer* tm, int cat) {
+  if (ld % 4 != 0) fail(SPLATT_ERR_BADINPUT, "internal: ld must be a multiple of 4");
+  const int chunk = mttkrp_chunk_leaves(c.N, ld);
+  ensure_chunk_table(ctx, c, chunk);
+  SB_CUDA(cudaMemsetAsync(out, 0, out_rows * (size_t)ld * sizeof(double), ctx->stream));
+  if (tm) tm->begin(cat);
+  switch (c.N) {
+    case 3: launch_n<3>(ctx, c, fac_by_mode, out, ld, R, chunk); break;
+    case 4: launch_n<4>(ctx, c, fac_by_mode, out, ld, R, chunk); break;
+    case 5: launch_n<5>(ctx, c, fac_by_mode, out, ld, R, chunk); break;
+    case 6: launch_n<6>(ctx, c, fac_by_mode, out, ld, R, chunk); break;
+    case 7: launch_n<7>(ctx, c, fac_by_mode, out, ld, R, chunk); break;
+    case 8: launch_n<8>(ctx, c, fac_by_mode, out, ld, R, chunk); break;
+    default: fail(SPLATT_ERR_BADINPUT, "nmodes out of range");
+  }
+  if (tm) tm->end();
+}
+
+}  // namespace sb

@@ -1,0 +1,269 @@
+"""GPU parity through the C ABI against the CPU oracle (gpu-marked).
+
+Bars (BASELINE.json north star):
+  CSF          bit-exact (ids, ptr, vals)                      — integer work
+  MTTKRP       ||M_gpu - M_orc||_F / ||M_orc||_F <= 1e-10      — fp64, summation order only
+               bit-exact on integer inputs (every partial sum is exact)
+  CP-ALS       factors / lambda / fit <= 1e-7 relative after a fixed iteration count
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests.gpu_util import ALS_TOL, MTTKRP_TOL, dev_coo, dev_factors, rel_fro
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sb(cuda_ok):
+    from paper_1812_05961_b200 import build
+    build.build()
+    import paper_1812_05961_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(sb):
+    return sb.Context(0)
+
+
+def check_csf_equal(csf, t):
+    for n in range(t.nmodes):
+        g = csf.export(n)
+        o = oracle.csf_build(t.dims, t.ind, t.vals, n)
+        assert g["perm"] == o["perm"].tolist()
+        for l in range(t.nmodes):
+            assert np.array_equal(g["ids"][l], o["ids"][l]), (n, l)
+        for l in range(t.nmodes - 1):
+            assert np.array_equal(g["ptr"][l], o["ptr"][l]), (n, l)
+        assert np.array_equal(g["vals"].view(np.uint64), o["vals"].view(np.uint64))
+
+
+def scaled_tensors():
+    """Parity-size tensors with the configs' distributions, spanning many chunks."""
+    out = [synth.generate_config("c1")]
+    out.append(synth.generate((40_000, 11_000, 75_000), 300_000, [("zipf", 1.1)] * 3, "ratings",
+                              seed=22))
+    out.append(synth.generate((48_000, 1_800, 200), 250_000,
+                              [("zipf", 1.0), ("zipf", 1.2), ("uniform",)], "ratings", seed=33))
+    out.append(synth.generate((1_200, 900, 2_900), 200_000, [("uniform",)] * 3, "lognormal",
+                              seed=44))
+    out.append(synth.generate((20_000, 5_000, 1_000, 50), 300_000, [("zipf", 1.05)] * 4, "u01",
+                              seed=55))
+    return out
+
+
+TENSORS = None
+
+
+def tensors():
+    global TENSORS
+    if TENSORS is None:
+        TENSORS = scaled_tensors()
+    return TENSORS
+
+
+# ------------------------------------------------------------------- CSF
+def test_csf_bit_exact_random_small(sb, ctx):
+    for seed in range(40):
+        N = 3 + seed % 3
+        t = synth.random_tiny(seed, nmodes=N, max_dim=9, max_nnz=120, dups=(seed % 2 == 0))
+        ind, vals = dev_coo(t)
+        csf = sb.csf_build(ind, vals, t.dims, ctx=ctx)
+        check_csf_equal(csf, t)
+
+
+def test_csf_bit_exact_config_shaped(sb, ctx):
+    for t in tensors():
+        ind, vals = dev_coo(t)
+        csf = sb.csf_build(ind, vals, t.dims, ctx=ctx)
+        check_csf_equal(csf, t)
+
+
+def test_csf_host_input_and_wide_keys(sb, ctx):
+    # host COO path + a key wider than 64 bits (8 modes x 2^9+ dims -> multi-group sort)
+    rng = np.random.default_rng(3)
+    dims = (700, 600, 900, 1000, 513, 800, 650, 1023)
+    nnz = 3000
+    ind = [rng.integers(0, d, nnz).astype(np.uint32) for d in dims]
+    vals = rng.random(nnz)
+    t = synth.SparseTensor(dims, ind, vals)
+    csf = sb.csf_build(ind, vals, dims, ctx=ctx)
+    check_csf_equal(csf, t)
+
+
+# ---------------------------------------------------------------- MTTKRP
+def run_mttkrp(sb, ctx, t, F, mode, ld=None, pad_value=0.0):
+    ind, vals = dev_coo(t)
+    csf = sb.csf_build(ind, vals, t.dims, ctx=ctx)
+    R = F[0].shape[1]
+    fd = dev_factors(F, ld=ld, pad_value=pad_value)
+    out = sb.mttkrp(csf, mode, fd, rank=R)
+    ctx.sync()
+    return out.cpu().numpy()[:, :R], out.cpu().numpy()
+
+
+@pytest.mark.parametrize("R", [1, 3, 8, 16, 35, 64])
+def test_mttkrp_parity_config_shaped(sb, ctx, R):
+    rng = np.random.default_rng(R)
+    for t in tensors():
+        F = [rng.standard_normal((d, R)) for d in t.dims]
+        ind, vals = dev_coo(t)
+        csf = sb.csf_build(ind, vals, t.dims, ctx=ctx)
+        ld = sb.padded_ld(R)
+        fd = dev_factors(F, ld=ld)
+        for n in range(t.nmodes):
+            M = sb.mttkrp(csf, n, fd, rank=R).cpu().numpy()
+            ref = oracle.mttkrp(t.dims, t.ind, t.vals, F, n)
+            assert rel_fro(M[:, :R], ref) <= MTTKRP_TOL, (t.dims, R, n)
+            assert np.all(M[:, R:] == 0)
+
+
+def test_mttkrp_integer_bit_exact(sb, ctx):
+    """X-3: integer values x factors in {0,1,2}: exact in fp64 in any order."""
+    rng = np.random.default_rng(11)
+    for t in tensors()[1:3]:
+        F = [rng.integers(0, 3, (d, 35)).astype(np.float64) for d in t.dims]
+        for n in range(t.nmodes):
+            M, _ = run_mttkrp(sb, ctx, t, F, n, ld=36)
+            assert np.array_equal(M, oracle.mttkrp(t.dims, t.ind, t.vals, F, n))
+
+
+def test_mttkrp_random_small_all_modes_and_ranks(sb, ctx):
+    for seed in range(30):
+        N = 3 + seed % 3
+        t = synth.random_tiny(100 + seed, nmodes=N, max_dim=9, max_nnz=200, dups=(seed % 3 == 0))
+        rng = np.random.default_rng(seed)
+        R = int(rng.integers(1, 40))
+        F = [rng.standard_normal((d, R)) for d in t.dims]
+        for n in range(N):
+            M, _ = run_mttkrp(sb, ctx, t, F, n)
+            assert rel_fro(M, oracle.mttkrp(t.dims, t.ind, t.vals, F, n)) <= MTTKRP_TOL
+
+
+def test_mttkrp_heavy_slice_and_long_fiber(sb, ctx):
+    """One slice spanning hundreds of chunks (fp64 atomics at chunk seams) and a fiber
+    longer than a chunk; plus many singleton slices."""
+    rng = np.random.default_rng(5)
+    I0, I1, I2 = 50, 40, 30_000
+    a = [np.zeros(20_000, np.uint32), rng.integers(0, I1, 20_000).astype(np.uint32),
+         rng.permutation(I2)[:20_000].astype(np.uint32)]
+    a[1][:5000] = 7  # one long fiber (slice 0, j = 7)
+    b = [rng.integers(1, I0, 3000).astype(np.uint32), rng.integers(0, I1, 3000).astype(np.uint32),
+         rng.integers(0, I2, 3000).astype(np.uint32)]
+    coords = np.unique(np.stack([np.concatenate([a[m], b[m]]) for m in range(3)], 1), axis=0)
+    coords = coords[rng.permutation(len(coords))]
+    t = synth.SparseTensor((I0, I1, I2), [coords[:, m].copy() for m in range(3)],
+                           rng.random(len(coords)))
+    F = [rng.standard_normal((d, 35)) for d in t.dims]
+    for n in range(3):
+        M, _ = run_mttkrp(sb, ctx, t, F, n)
+        assert rel_fro(M, oracle.mttkrp(t.dims, t.ind, t.vals, F, n)) <= MTTKRP_TOL
+
+
+def test_mttkrp_ld_variants_and_garbage_pads(sb, ctx):
+    t = tensors()[1]
+    rng = np.random.default_rng(2)
+    R = 35
+    F = [rng.standard_normal((d, R)) for d in t.dims]
+    ref = oracle.mttkrp(t.dims, t.ind, t.vals, F, 0)
+    for ld, pad in ((35, 0.0), (36, np.nan), (40, 7.0), (37, 1e300)):
+        M, full = run_mttkrp(sb, ctx, t, F, 0, ld=ld, pad_value=pad)
+        assert rel_fro(M, ref) <= MTTKRP_TOL, ld
+        assert np.all(full[:, R:] == 0), ld
+
+
+def test_mttkrp_empty_rows_are_zero(sb, ctx):
+    t = synth.generate((5000, 300, 200), 2000, [("zipf", 1.2)] * 3, "u01", seed=9)
+    rng = np.random.default_rng(0)
+    F = [rng.random((d, 8)) for d in t.dims]
+    M, _ = run_mttkrp(sb, ctx, t, F, 0)
+    empty = np.setdiff1d(np.arange(5000), t.ind[0])
+    assert empty.size > 0 and np.all(M[empty] == 0)
+
+
+# ----------------------------------------------------------------- CP-ALS
+def als_compare(res, ref, tol=ALS_TOL):
+    for n, (A, B) in enumerate(zip(res["factors"], ref["factors"])):
+        A = A.cpu().numpy() if hasattr(A, "cpu") else A
+        assert rel_fro(A, B) <= tol, ("factor", n, rel_fro(A, B))
+    lam = res["lam"].cpu().numpy() if hasattr(res["lam"], "cpu") else res["lam"]
+    assert rel_fro(lam, ref["lam"]) <= tol
+    assert abs(res["fit"] - ref["fit"]) <= tol * abs(ref["fit"])
+    assert res["iters"] == ref["iters"]
+    assert np.allclose(res["fit_history"], ref["fit_history"], rtol=tol, atol=0)
+
+
+def test_cpd_als_c1_full_parity(sb, ctx):
+    t = synth.generate_config("c1")
+    ind, vals = dev_coo(t)
+    res = sb.cpd_als(ind, vals, t.dims, rank=8, max_iters=10, tol=0.0, seed=1, ctx=ctx)
+    ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=8, max_iters=10, tol=0.0, seed=1)
+    als_compare(res, ref)
+
+
+@pytest.mark.parametrize("idx,R,iters", [(1, 35, 5), (2, 35, 5), (3, 64, 3), (4, 16, 5)])
+def test_cpd_als_config_shaped_parity(sb, ctx, idx, R, iters):
+    t = tensors()[idx]
+    ind, vals = dev_coo(t)
+    res = sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=iters, seed=idx, ctx=ctx)
+    ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=R, max_iters=iters, seed=idx)
+    als_compare(res, ref)
+
+
+def test_cpd_als_one_step_from_oracle_state(sb, ctx):
+    """Each GPU iteration started from the oracle's factors: isolates kernel error
+    from the ALS amplification of rounding (last row)."""
+    t = tensors()[1]
+    R = 35
+    A = oracle.init_factors(t.dims, R, 7)
+    ind, vals = dev_coo(t)
+    for step in range(3):
+        ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=R, max_iters=1, init=A)
+        res = sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=1, init=A, ctx=ctx)
+        als_compare(res, ref, tol=1e-9)
+        A = [f * 1.0 for f in ref["factors"]]
+
+
+def test_cpd_als_rank1_planted_and_host_io(sb, ctx):
+    rng = np.random.default_rng(4)
+    F = [rng.random((d, 1)) + 0.1 for d in (9, 7, 8)]
+    t = synth.full_kruskal(F)
+    res = sb.cpd_als(t.ind, t.vals, t.dims, rank=1, max_iters=1, seed=3, ctx=ctx, out_device=False)
+    assert 0.0 <= 1.0 - res["fit"] <= 1e-7
+    for n in range(3):
+        a = res["factors"][n][:, 0] / np.linalg.norm(res["factors"][n][:, 0])
+        b = F[n][:, 0] / np.linalg.norm(F[n][:, 0])
+        assert np.max(np.abs(a - b)) <= 1e-12
+
+
+def test_cpd_als_tol_stops_like_oracle(sb, ctx):
+    t = tensors()[0]
+    ind, vals = dev_coo(t)
+    res = sb.cpd_als(ind, vals, t.dims, rank=8, max_iters=100, tol=1e-4, seed=1, ctx=ctx)
+    ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=8, max_iters=100, tol=1e-4, seed=1)
+    assert res["iters"] == ref["iters"] < 100
+    als_compare(res, ref)
+
+
+def test_errors(sb, ctx):
+    t = synth.random_tiny(3)
+    ind, vals = dev_coo(t)
+    with pytest.raises(ValueError):
+        sb.cpd_als(ind, vals, t.dims, rank=0, max_iters=1, ctx=ctx)
+    with pytest.raises(ValueError):
+        sb.cpd_als(ind, vals, t.dims, rank=2, max_iters=0, ctx=ctx)
+    with pytest.raises(sb.EmptyTensorError):
+        sb.cpd_als(ind, vals * 0, t.dims, rank=2, max_iters=1, ctx=ctx)
+    bad = [a.clone() for a in ind]
+    bad[1][0] = t.dims[1]
+    with pytest.raises(sb.BadInputError):
+        sb.cpd_als(bad, vals, t.dims, rank=2, max_iters=1, ctx=ctx)
+    with pytest.raises(sb.BadInputError):
+        sb.csf_build(bad, vals, t.dims, ctx=ctx)
+    zero = [np.zeros((d, 3)) for d in t.dims]
+    with pytest.raises(sb.SingularError):
+        sb.cpd_als(ind, vals, t.dims, rank=3, max_iters=1, init=zero, ctx=ctx)
+    ctx.sync()  # context still healthy after the errors
