@@ -103,8 +103,9 @@ typedef struct {
 
 /* ---------------------------------------------------------------- context */
 /* Create a context on CUDA device `device`.  cuda_stream: a cudaStream_t to order
- * all work on (e.g. torch.cuda.current_stream().cuda_stream), or NULL for a
- * library-owned non-blocking stream.  *out is set only on success.              */
+ * all work on (e.g. torch.cuda.current_stream().cuda_stream; pass cudaStreamLegacy,
+ * i.e. (void*)1, for the legacy default stream), or NULL for a library-owned
+ * non-blocking stream.  *out is set only on success.                             */
 splatt_status splatt_ctx_create(splatt_ctx** out, int device, void* cuda_stream);
 void          splatt_ctx_destroy(splatt_ctx* ctx);
 /* Wait for all work on the context stream; reports asynchronous faults.         */

@@ -26,6 +26,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsplatt_b200.so")
 MAX_NMODES = 8
 MAX_RANK = 128
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
 
 STATUS = {0: "OK", -1: "BADINPUT", -2: "NOMEM", -3: "SINGULAR", -4: "CUDA", -5: "NCCL",
           -6: "EMPTY", -7: "UNSUPPORTED"}
@@ -150,6 +151,8 @@ class Context:
             stream = torch.cuda.current_stream(self.device)
         self.stream = stream
         handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        if handle == 0:  # torch's default stream is the legacy default stream
+            handle = CUDA_STREAM_LEGACY
         p = C.c_void_p()
         _raise(lib().splatt_ctx_create(C.byref(p), self.device, C.c_void_p(handle)))
         self._p = p

@@ -76,12 +76,13 @@ __global__ void sum_partials_kernel(const double* __restrict__ part, int P, doub
   if (threadIdx.x == 0) out[0] = s;
 }
 
-// One CTA.  smem: V (R*R) and W (R*R; L is built in W's lower triangle).
+// One CTA.  smem: W (R*R) = V; L is built in W's lower triangle while the strict upper
+// triangle keeps V (V is exactly symmetric), and diag keeps V's diagonal for the retry.
 __global__ void hadamard_cholesky_kernel(const double* __restrict__ G_all, int N, int n, int R,
                                          double* __restrict__ L, int* status) {
   extern __shared__ double sm[];
-  double* V = sm;
-  double* W = sm + R * R;
+  double* W = sm;
+  double* diag = sm + R * R;
   __shared__ int failed;
   __shared__ double thr, ridge;
   const int RR = R * R;
@@ -94,7 +95,8 @@ __global__ void hadamard_cholesky_kernel(const double* __restrict__ G_all, int N
       p = first ? g : p * g;
       first = false;
     }
-    V[e] = p;
+    W[e] = p;
+    if (e / R == e % R) diag[e / R] = p;
   }
   __syncthreads();
   for (int attempt = 0; attempt < 2; ++attempt) {
@@ -102,15 +104,18 @@ __global__ void hadamard_cholesky_kernel(const double* __restrict__ G_all, int N
       failed = 0;
       if (attempt == 1) {
         double tr = 0.0;
-        for (int j = 0; j < R; ++j) tr += V[j * R + j];
+        for (int j = 0; j < R; ++j) tr += diag[j];
         ridge = 1e-12 * tr / R;
       } else {
         ridge = 0.0;
       }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < RR; e += blockDim.x)
-      W[e] = V[e] + ((e / R == e % R) ? ridge : 0.0);
+    for (int e = threadIdx.x; e < RR; e += blockDim.x) {
+      const int i = e / R, j = e % R;
+      if (i == j) W[e] = diag[i] + ridge;
+      else if (i > j) W[e] = W[j * R + i];  // restore the lower triangle from the upper
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
       double mx = 0.0;
@@ -371,11 +376,12 @@ void norm_sq(splatt_ctx* ctx, const double* vals, uint64_t nnz, double* d_out) {
 
 void hadamard_cholesky(splatt_ctx* ctx, const double* G_all, int N, int n, int R, double* L,
                        int* status) {
-  const size_t smem = 2 * (size_t)R * R * sizeof(double);
+  const size_t smem = ((size_t)R * R + R) * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
     SB_CUDA(cudaFuncSetAttribute(hadamard_cholesky_kernel,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 128 * 128 * 8));
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (128 * 128 + 128) * 8));
     attr_set = true;
   }
   hadamard_cholesky_kernel<<<1, kThreads, smem, ctx->stream>>>(G_all, N, n, R, L, status);
