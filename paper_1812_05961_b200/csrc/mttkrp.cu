@@ -8,18 +8,19 @@
 //    group of G lanes (G = next pow2 of ld/4; each lane owns 4 consecutive columns
 //    and moves them with one 256-bit load).  Fixed-size leaf chunks balance the
 //    power-law slices (a 13.8M-nonzero slice is just many chunks) — SURVEY.md §8(a')1a.
-//  * A group walks its chunk in batches of 32 leaves.  Per batch it loads windows of
-//    leaf ids/values (streamed, L1 no-allocate) and of every internal level's ptr,
-//    turns them into 32-bit "node closes here" masks (segment flags derived from ptr,
-//    §8(a')2), and then runs the leaves sequentially with register accumulators per
-//    level: leaf rows are FMA'd into the fiber accumulator, a closing node multiplies
-//    its accumulator by its own factor row and pushes it one level up, and a closing
-//    slice writes its output row.
-//  * Rows in flight: the U leaf rows (and the rows of the nodes they close) of a
-//    sub-batch are all issued before any is consumed (Little's law, §8(a')4).
-//  * Slices wholly inside a chunk are written with plain 256-bit stores (conflict-
-//    free: rows are owned); the <= 2 slices per chunk that cross a chunk boundary are
-//    accumulated with fp64 atomics into the zero-filled output.
+//  * A group walks its chunk in batches of 32 leaves.  Per batch, lane-parallel: load
+//    windows of leaf ids/values (streamed, L1 no-allocate) and of every internal
+//    level's ptr, turn them into 32-bit "node closes here" masks (segment flags derived
+//    from ptr, §8(a')2), and resolve for every leaf how many levels it closes and the
+//    ids of the closed nodes; the result goes to a per-group shared-memory table.
+//  * Then the group runs the batch's leaves in order with register accumulators per
+//    level: a leaf row is FMA'd into the fiber accumulator; a closing node multiplies
+//    its accumulator by its own factor row and pushes it one level up; a closing slice
+//    writes its output row.  The rows of U leaves (and of the nodes they close) are
+//    issued before any is consumed (Little's law, §8(a')4).
+//  * Slices wholly inside a chunk are written with plain 256-bit stores (conflict-free:
+//    rows are owned); the <= 2 slices per chunk that cross a chunk seam are accumulated
+//    with fp64 atomics into the zero-filled output (outside the per-leaf loop).
 #include <algorithm>
 
 #include "csf.hpp"
@@ -39,7 +40,8 @@ struct Args {
   double* out;
   const uint32_t* tab;
   uint32_t nnz, nchunks, chunk;
-  int ld, R;
+  uint32_t ld;
+  int R;
 };
 
 struct d4 { double x, y, z, w; };
@@ -47,7 +49,7 @@ struct d4 { double x, y, z, w; };
 __device__ __forceinline__ d4 ldg_row(const double* p) {
   d4 r;
   asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
-               : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+      : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
   return r;
 }
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
@@ -101,18 +103,45 @@ __device__ __forceinline__ void fma4v(d4& acc, const d4& a, const d4& r) {
   acc.w = fma(a.w, r.w, acc.w);
 }
 
+// Per-leaf record written by the lane-parallel phase.  Word 0: leaf factor row id;
+// word 1: closing depth d (levels d..N-2 close at this leaf; N-1 = none) | 0x100 if the
+// closing slice is the chunk's first slice and began in an earlier chunk (-> atomic);
+// word 2: output row (if d == 0); words 3..: ids of the closed nodes at levels 1..N-2.
+template <int N>
+struct MetaLayout {
+  static constexpr int kWords = ((3 + (N - 2)) + 3) / 4 * 4;
+  static constexpr int kVec = kWords / 4;
+};
+
+constexpr int kBatch = 32;
+constexpr int kBlock = 256;
+
+template <int N>
+__host__ __device__ constexpr int group_smem_words() {
+  return MetaLayout<N>::kWords * kBatch + 2 * kBatch;  // meta + values (doubles)
+}
+
 // NM = N-2 internal levels below the root that carry factor rows (>= 1 for N >= 3).
 template <int N, int G, int U>
-__global__ void __launch_bounds__(256) mttkrp_root_kernel(const Args<N> a) {
-  constexpr int E = 32 / G;  // window entries per lane
+__global__ void __launch_bounds__(kBlock) mttkrp_root_kernel(const Args<N> a) {
+  constexpr int E = kBatch / G;  // window entries per lane
   constexpr int NM = N - 2;
+  constexpr int MV = MetaLayout<N>::kVec;
+  extern __shared__ __align__(16) uint32_t smem[];
   const int lane = threadIdx.x & 31;
   const int q = lane & (G - 1);
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  const uint32_t gib = threadIdx.x / G;  // group in block
+  uint32_t* gs = smem + gib * group_smem_words<N>();
+  uint4* meta = reinterpret_cast<uint4*>(gs);
+  double* sval = reinterpret_cast<double*>(gs + MetaLayout<N>::kWords * kBatch);
   const uint32_t group = (blockIdx.x * blockDim.x + threadIdx.x) / G;
   const uint32_t ngroups = gridDim.x * blockDim.x / G;
-  const bool active = 4 * q < a.ld;
-  const int col = 4 * q;
+  const bool active = 4u * q < a.ld;
+  const uint32_t col = 4u * q;
+  // Idle lanes (4q >= ld) re-read column 0..3 so every load is unconditional and valid.
+  const uint32_t colc = active ? col : 0u;
+  const double* __restrict__ fleaf = a.fac[N - 1] + colc;
 
   for (uint32_t c = group; c < a.nchunks; c += ngroups) {
     const uint32_t k0 = c * a.chunk;
@@ -125,24 +154,14 @@ __global__ void __launch_bounds__(256) mttkrp_root_kernel(const Args<N> a) {
     d4 acc[N - 1];
 #pragma unroll
     for (int l = 0; l < N - 1; ++l) acc[l] = d4{0, 0, 0, 0};
+    d4 pending = d4{0, 0, 0, 0};  // first slice, begun in an earlier chunk
+    bool has_pending = false;
+    uint32_t pending_row = 0;
     int last_dep = N - 1;
 
-    for (uint32_t kb = k0; kb < k1; kb += 32) {
-      const uint32_t nb = min(32u, k1 - kb);
-      uint32_t lid[E];
-      double lv[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const uint32_t t = q + e * G;
-        lid[e] = 0;
-        lv[e] = 0.0;
-        if (t < nb) {
-          lid[e] = ld_stream_u32(a.ids[N - 1] + kb + t);
-          lv[e] = ld_stream_f64(a.vals + kb + t);
-        }
-      }
-      // Close masks.  msk[N-2]: bit t = leaf kb+t is the last child of its level-(N-2)
-      // node.  msk[l] (l < N-2): bit u = level-(l+1) node base[l+1]+u is a last child.
+    for (uint32_t kb = k0; kb < k1; kb += kBatch) {
+      const uint32_t nb = min((uint32_t)kBatch, k1 - kb);
+      // ---- lane-parallel phase: masks, then one record per leaf into shared memory
       uint32_t msk[N - 1];
       {
         uint32_t m = 0;
@@ -175,97 +194,108 @@ __global__ void __launch_bounds__(256) mttkrp_root_kernel(const Args<N> a) {
       for (int l = N - 3; l >= 0; --l) cnt[l] = __popc(msk[l] & lowmask(cnt[l + 1]));
 
 #pragma unroll
-      for (int sb = 0; sb < 32; sb += U) {
-        if ((uint32_t)sb < nb) {
-          d4 row[U];
-          d4 mid[U][NM];
-          double v[U];
-          int dep[U];
-          uint32_t nodei[U][N - 1];
-          uint32_t rid[U];
-          // phase 1: closing chains and node ids
+      for (int e = 0; e < E; ++e) {
+        const uint32_t t = q + e * G;
+        uint32_t w[MetaLayout<N>::kWords];
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int t = sb + u;
-            const uint32_t id = __shfl_sync(gmask, lid[t / G], t % G, G);
-            v[u] = __shfl_sync(gmask, lv[t / G], t % G, G);
-            dep[u] = N - 1;
-            rid[u] = id;
-            if ((uint32_t)t < nb && ((msk[N - 2] >> t) & 1u)) {
-              uint32_t li = __popc(msk[N - 2] & lowmask(t));
-              nodei[u][N - 2] = base[N - 2] + li;
-              dep[u] = N - 2;
+        for (int z = 0; z < MetaLayout<N>::kWords; ++z) w[z] = 0u;
+        double v = 0.0;
+        uint32_t dep = N - 1;
+        if (t < nb) {
+          w[0] = ld_stream_u32(a.ids[N - 1] + kb + t);
+          v = ld_stream_f64(a.vals + kb + t);
+          if ((msk[N - 2] >> t) & 1u) {
+            uint32_t li = __popc(msk[N - 2] & lowmask(t));
+            uint32_t node = base[N - 2] + li;
+            dep = N - 2;
+            if (NM >= 1) w[3 + (N - 2) - 1] = a.ids[N - 2][node];
 #pragma unroll
-              for (int l = N - 3; l >= 0; --l) {
-                if (dep[u] == l + 1 && ((msk[l] >> li) & 1u)) {
-                  li = __popc(msk[l] & lowmask(li));
-                  nodei[u][l] = base[l] + li;
-                  dep[u] = l;
+            for (int l = N - 3; l >= 0; --l) {
+              if (dep == (uint32_t)(l + 1) && ((msk[l] >> li) & 1u)) {
+                li = __popc(msk[l] & lowmask(li));
+                node = base[l] + li;
+                dep = l;
+                if (l >= 1) w[3 + l - 1] = a.ids[l][node];
+                else {
+                  w[2] = a.ids[0][node];
+                  if (first_partial && node == slice0) dep |= 0x100u;
                 }
               }
             }
           }
-          // phase 2: ids of the closing nodes (factor row ids / output row)
-          uint32_t nid[U][NM];
-          uint32_t oid[U];
+        }
+        w[1] = dep;
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
+        for (int z = 0; z < MV; ++z)
+          meta[t * MV + z] = make_uint4(w[4 * z], w[4 * z + 1], w[4 * z + 2], w[4 * z + 3]);
+        sval[t] = v;
+      }
+      __syncwarp(gmask);
+
+      // ---- sequential phase: U leaves at a time, all row loads issued first
+      for (uint32_t t0 = 0; t0 < nb; t0 += U) {
+        d4 row[U];
+        d4 mid[U][NM];
+        uint32_t dep[U], orow[U];
+        double v[U];
 #pragma unroll
-            for (int l = 1; l <= NM; ++l) nid[u][l - 1] = dep[u] <= l ? a.ids[l][nodei[u][l]] : 0u;
-            oid[u] = dep[u] == 0 ? a.ids[0][nodei[u][0]] : 0u;
+        for (int u = 0; u < U; ++u) {
+          const uint32_t t = t0 + u;
+          uint32_t w[MetaLayout<N>::kWords];
+#pragma unroll
+          for (int z = 0; z < MV; ++z) {
+            const uint4 m4 = meta[t * MV + z];
+            w[4 * z] = m4.x; w[4 * z + 1] = m4.y; w[4 * z + 2] = m4.z; w[4 * z + 3] = m4.w;
           }
-          // phase 3: issue every row load of the sub-batch before consuming any
+          v[u] = sval[t];
+          dep[u] = w[1];
+          orow[u] = w[2];
+          row[u] = ldg_row(fleaf + (size_t)w[0] * a.ld);
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int t = sb + u;
-            row[u] = d4{0, 0, 0, 0};
-            if ((uint32_t)t < nb && active)
-              row[u] = ldg_row(a.fac[N - 1] + (size_t)rid[u] * a.ld + col);
+          for (int l = 1; l <= NM; ++l)
+            if ((w[1] & 0xffu) <= (uint32_t)l)
+              mid[u][l - 1] = ldg_row(a.fac[l] + colc + (size_t)w[3 + l - 1] * a.ld);
+        }
 #pragma unroll
-            for (int l = 1; l <= NM; ++l) {
-              mid[u][l - 1] = d4{0, 0, 0, 0};
-              if (dep[u] <= l && active)
-                mid[u][l - 1] = ldg_row(a.fac[l] + (size_t)nid[u][l - 1] * a.ld + col);
+        for (int u = 0; u < U; ++u) {
+          if (t0 + u < nb) {
+            const uint32_t d = dep[u] & 0xffu;
+            fma4(acc[N - 2], v[u], row[u]);
+#pragma unroll
+            for (int l = NM; l >= 1; --l) {
+              if (d <= (uint32_t)l) {
+                fma4v(acc[l - 1], acc[l], mid[u][l - 1]);
+                acc[l] = d4{0, 0, 0, 0};
+              }
             }
-          }
-          // phase 4: accumulate, push closed nodes up, write closed slices
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int t = sb + u;
-            if ((uint32_t)t < nb) {
-              fma4(acc[N - 2], v[u], row[u]);
-              const int d = dep[u];
-#pragma unroll
-              for (int l = NM; l >= 1; --l) {
-                if (d <= l) {
-                  fma4v(acc[l - 1], acc[l], mid[u][l - 1]);
-                  acc[l] = d4{0, 0, 0, 0};
-                }
+            if (d == 0) {
+              if (dep[u] & 0x100u) {
+                pending = acc[0];
+                pending_row = orow[u];
+                has_pending = true;
+              } else if (active) {
+                st_row(a.out + (size_t)orow[u] * a.ld + col, mask_pad(acc[0], col, a.R));
               }
-              if (d == 0) {
-                if (active) {
-                  double* o = a.out + (size_t)oid[u] * a.ld + col;
-                  const d4 w = mask_pad(acc[0], col, a.R);
-                  if (first_partial && nodei[u][0] == slice0) atomic_row(o, w);
-                  else st_row(o, w);
-                }
-                acc[0] = d4{0, 0, 0, 0};
-              }
-              last_dep = d;
+              acc[0] = d4{0, 0, 0, 0};
             }
           }
         }
       }
+      last_dep = (int)(meta[(nb - 1) * MV].y & 0xffu);
+      __syncwarp(gmask);
 #pragma unroll
       for (int l = 0; l < N - 1; ++l) base[l] += cnt[l];
     }
-    // Chunk end: fold the still-open levels (< last_dep) into the open slice's row.
+    // Chunk seams: the first slice (if it began earlier) and the still-open levels
+    // (< last_dep) of the last slice go out through fp64 atomics.
+    if (has_pending && active)
+      atomic_row(a.out + (size_t)pending_row * a.ld + col, mask_pad(pending, col, a.R));
     if (last_dep > 0) {
 #pragma unroll
       for (int l = NM; l >= 1; --l) {
-        if (l < last_dep && active) {
+        if (l < last_dep) {
           const uint32_t nid = a.ids[l][base[l]];
-          const d4 r = ldg_row(a.fac[l] + (size_t)nid * a.ld + col);
+          const d4 r = ldg_row(a.fac[l] + colc + (size_t)nid * a.ld);
           fma4v(acc[l - 1], acc[l], r);
         }
       }
@@ -293,11 +323,24 @@ void launch_t(splatt_ctx* ctx, const DevCsf& c, const double* const* fac_by_mode
   a.nnz = (uint32_t)c.nnz;
   a.nchunks = (uint32_t)c.nchunks;
   a.chunk = (uint32_t)chunk;
-  a.ld = ld;
+  a.ld = (uint32_t)ld;
   a.R = R;
-  const uint64_t groups_per_block = 256 / G;
+  // 256 threads per block unless the per-group tables would exceed 160 KB (many small
+  // groups with many levels); the kernel indexes groups by blockDim, not kBlock.
+  int threads = kBlock;
+  while (threads > 64 && (size_t)(threads / G) * group_smem_words<N>() * 4 > 160 * 1024)
+    threads /= 2;
+  const int groups_per_block = threads / G;
+  const size_t smem = (size_t)groups_per_block * group_smem_words<N>() * 4;
+  static bool attr = false;
+  if (!attr) {
+    SB_CUDA(cudaFuncSetAttribute(mttkrp_root_kernel<N, G, U>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    attr = true;
+  }
   const uint64_t blocks = ceil_div(c.nchunks, groups_per_block);
-  mttkrp_root_kernel<N, G, U><<<(unsigned)std::max<uint64_t>(1, blocks), 256, 0, ctx->stream>>>(a);
+  mttkrp_root_kernel<N, G, U>
+      <<<(unsigned)std::max<uint64_t>(1, blocks), threads, smem, ctx->stream>>>(a);
   SB_CHECK_LAUNCH(ctx);
 }
 
@@ -323,9 +366,8 @@ int mttkrp_chunk_leaves(int N, int ld) {
 
 double mttkrp_alg_bytes(const DevCsf& c, int R) {
   // B_alg = CSF index/value bytes + gathered factor-row bytes:
-  // 12 B per leaf (id + value), 8 B per internal node (id + ptr) except the root level
-  // (8 B per slice: id + ptr), plus 8 R bytes per gathered row (one per leaf and one
-  // per internal node below the root).
+  // 12 B per leaf (id + value), 8 B per internal node (id + ptr) and per slice, plus
+  // 8 R bytes per gathered row (one per leaf and one per internal node below the root).
   double nodes_below_root = 0.0;
   for (int l = 1; l < c.N - 1; ++l) nodes_below_root += (double)c.nodes[l];
   const double nnz = (double)c.nnz;
