@@ -23,7 +23,7 @@ __all__ = ["lib", "Context", "Csf", "csf_build", "mttkrp", "cpd_als", "partition
            "SplattError", "SingularError", "EmptyTensorError", "STATUS", "padded_ld"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsplatt_b200.so")
+LIB_PATH = os.environ.get("SPLATT_B200_LIB") or os.path.join(_HERE, "libsplatt_b200.so")
 MAX_NMODES = 8
 MAX_RANK = 128
 CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy

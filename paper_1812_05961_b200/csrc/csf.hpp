@@ -22,6 +22,7 @@ struct DevCsf {
   int tab_chunk = 0;
   uint64_t nchunks = 0;
   DevBuf<uint32_t> tab;
+  DevBuf<double> seam;  // MTTKRP scratch: one row per chunk (chunk-seam slices)
 };
 
 // perm: root first, then the other modes by ascending length, ties to the lower id

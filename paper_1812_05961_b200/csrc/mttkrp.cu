@@ -39,6 +39,7 @@ struct Args {
   const double* vals;
   double* out;
   const uint32_t* tab;
+  double* seam;               // nchunks x ld: the chunk's first slice when it began earlier
   uint32_t nnz, nchunks, chunk;
   uint32_t ld;
   int R;
@@ -105,7 +106,8 @@ __device__ __forceinline__ void fma4v(d4& acc, const d4& a, const d4& r) {
 
 // Per-leaf record written by the lane-parallel phase.  Word 0: leaf factor row id;
 // word 1: closing depth d (levels d..N-2 close at this leaf; N-1 = none) | 0x100 if the
-// closing slice is the chunk's first slice and began in an earlier chunk (-> atomic);
+// closing slice is the chunk's first slice and began in an earlier chunk (its row goes
+// to the chunk's seam row and is added to the output with atomics at the chunk end);
 // word 2: output row (if d == 0); words 3..: ids of the closed nodes at levels 1..N-2.
 template <int N>
 struct MetaLayout {
@@ -122,8 +124,8 @@ __host__ __device__ constexpr int group_smem_words() {
 }
 
 // NM = N-2 internal levels below the root that carry factor rows (>= 1 for N >= 3).
-template <int N, int G, int U>
-__global__ void __launch_bounds__(kBlock) mttkrp_root_kernel(const Args<N> a) {
+template <int N, int G, int U, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) mttkrp_root_kernel(const Args<N> a) {
   constexpr int E = kBatch / G;  // window entries per lane
   constexpr int NM = N - 2;
   constexpr int MV = MetaLayout<N>::kVec;
@@ -154,9 +156,6 @@ __global__ void __launch_bounds__(kBlock) mttkrp_root_kernel(const Args<N> a) {
     d4 acc[N - 1];
 #pragma unroll
     for (int l = 0; l < N - 1; ++l) acc[l] = d4{0, 0, 0, 0};
-    d4 pending = d4{0, 0, 0, 0};  // first slice, begun in an earlier chunk
-    bool has_pending = false;
-    uint32_t pending_row = 0;
     int last_dep = N - 1;
 
     for (uint32_t kb = k0; kb < k1; kb += kBatch) {
@@ -217,8 +216,8 @@ __global__ void __launch_bounds__(kBlock) mttkrp_root_kernel(const Args<N> a) {
                 dep = l;
                 if (l >= 1) w[3 + l - 1] = a.ids[l][node];
                 else {
-                  w[2] = a.ids[0][node];
-                  if (first_partial && node == slice0) dep |= 0x100u;
+                  if (first_partial && node == slice0) { dep |= 0x100u; w[2] = c; }
+                  else w[2] = a.ids[0][node];
                 }
               }
             }
@@ -269,13 +268,8 @@ __global__ void __launch_bounds__(kBlock) mttkrp_root_kernel(const Args<N> a) {
               }
             }
             if (d == 0) {
-              if (dep[u] & 0x100u) {
-                pending = acc[0];
-                pending_row = orow[u];
-                has_pending = true;
-              } else if (active) {
-                st_row(a.out + (size_t)orow[u] * a.ld + col, mask_pad(acc[0], col, a.R));
-              }
+              double* dst = (dep[u] & 0x100u) ? a.seam : a.out;
+              if (active) st_row(dst + (size_t)orow[u] * a.ld + col, mask_pad(acc[0], col, a.R));
               acc[0] = d4{0, 0, 0, 0};
             }
           }
@@ -288,8 +282,11 @@ __global__ void __launch_bounds__(kBlock) mttkrp_root_kernel(const Args<N> a) {
     }
     // Chunk seams: the first slice (if it began earlier) and the still-open levels
     // (< last_dep) of the last slice go out through fp64 atomics.
-    if (has_pending && active)
-      atomic_row(a.out + (size_t)pending_row * a.ld + col, mask_pad(pending, col, a.R));
+    if (first_partial && base[0] != slice0 && active) {  // the first slice closed here
+      const double* sp = a.seam + (size_t)c * a.ld + col;  // written by this same lane
+      const d4 r = d4{sp[0], sp[1], sp[2], sp[3]};
+      atomic_row(a.out + (size_t)a.ids[0][slice0] * a.ld + col, r);
+    }
     if (last_dep > 0) {
 #pragma unroll
       for (int l = NM; l >= 1; --l) {
@@ -307,8 +304,8 @@ __global__ void __launch_bounds__(kBlock) mttkrp_root_kernel(const Args<N> a) {
   }
 }
 
-template <int N, int G, int U>
-void launch_t(splatt_ctx* ctx, const DevCsf& c, const double* const* fac_by_mode, double* out,
+template <int N, int G, int U, int MINB>
+void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, double* out,
               int ld, int R, int chunk) {
   Args<N> a{};
   for (int l = 0; l < N; ++l) {
@@ -320,6 +317,8 @@ void launch_t(splatt_ctx* ctx, const DevCsf& c, const double* const* fac_by_mode
   a.vals = c.vals.p;
   a.out = out;
   a.tab = c.tab.p;
+  if (c.seam.n < c.nchunks * (size_t)ld) c.seam.alloc(c.nchunks * (size_t)ld, ctx->stream);
+  a.seam = c.seam.p;
   a.nnz = (uint32_t)c.nnz;
   a.nchunks = (uint32_t)c.nchunks;
   a.chunk = (uint32_t)chunk;
@@ -334,26 +333,34 @@ void launch_t(splatt_ctx* ctx, const DevCsf& c, const double* const* fac_by_mode
   const size_t smem = (size_t)groups_per_block * group_smem_words<N>() * 4;
   static bool attr = false;
   if (!attr) {
-    SB_CUDA(cudaFuncSetAttribute(mttkrp_root_kernel<N, G, U>,
+    SB_CUDA(cudaFuncSetAttribute(mttkrp_root_kernel<N, G, U, MINB>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     attr = true;
   }
   const uint64_t blocks = ceil_div(c.nchunks, groups_per_block);
-  mttkrp_root_kernel<N, G, U>
+  mttkrp_root_kernel<N, G, U, MINB>
       <<<(unsigned)std::max<uint64_t>(1, blocks), threads, smem, ctx->stream>>>(a);
   SB_CHECK_LAUNCH(ctx);
 }
 
+#ifndef SB_MTTKRP_U
+#define SB_MTTKRP_U 4
+#endif
+#ifndef SB_MTTKRP_MINB
+#define SB_MTTKRP_MINB 2
+#endif
+
 template <int N>
-void launch_n(splatt_ctx* ctx, const DevCsf& c, const double* const* f, double* out, int ld,
+void launch_n(splatt_ctx* ctx, DevCsf& c, const double* const* f, double* out, int ld,
               int R, int chunk) {
   const int slots = ld / 4;
-  constexpr int U = (N <= 4) ? 4 : 2;
-  if (slots <= 2) launch_t<N, 2, U>(ctx, c, f, out, ld, R, chunk);
-  else if (slots <= 4) launch_t<N, 4, U>(ctx, c, f, out, ld, R, chunk);
-  else if (slots <= 8) launch_t<N, 8, U>(ctx, c, f, out, ld, R, chunk);
-  else if (slots <= 16) launch_t<N, 16, U>(ctx, c, f, out, ld, R, chunk);
-  else launch_t<N, 32, U>(ctx, c, f, out, ld, R, chunk);
+  constexpr int U = (N <= 4) ? SB_MTTKRP_U : 2;
+  constexpr int MB = (N <= 3) ? SB_MTTKRP_MINB : 1;
+  if (slots <= 2) launch_t<N, 2, U, MB>(ctx, c, f, out, ld, R, chunk);
+  else if (slots <= 4) launch_t<N, 4, U, MB>(ctx, c, f, out, ld, R, chunk);
+  else if (slots <= 8) launch_t<N, 8, U, MB>(ctx, c, f, out, ld, R, chunk);
+  else if (slots <= 16) launch_t<N, 16, U, MB>(ctx, c, f, out, ld, R, chunk);
+  else launch_t<N, 32, U, MB>(ctx, c, f, out, ld, R, chunk);
 }
 
 }  // namespace
