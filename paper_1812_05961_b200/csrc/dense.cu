@@ -5,11 +5,11 @@
 // (line 6), Gram refresh, and the fit (line 13).  Readings: DESIGN.md §2 (C-7 pivot
 // threshold / ridge, C-8 norm schedule, C-10 fit identity).
 //
-// Fusion: the row solve reads each M row once from HBM and, while
-// the solved rows are still in shared memory, accumulates the partial Gram, the
-// column max |a| and the fit inner product, so lambda / G_n / the fit need no
-// further pass over A except the final column scaling.  Reductions run in a fixed
-// order (per-CTA partials, then a fixed-order sum), so results are deterministic.
+// Structure: one CTA factors V; the row solves run one row per thread
+// on a shared-memory tile and also return the fit inner
+// product <M_i, A_i> = |L^-1 M_i|^2 of every row; one pass over the solved rows gives
+// the partial Gram and column max |a|; partials are reduced in a fixed order, so every
+// result is deterministic.
 #include <algorithm>
 #include <cmath>
 
@@ -150,19 +150,79 @@ __global__ void hadamard_cholesky_kernel(const double* __restrict__ G_all, int N
   if (threadIdx.x == 0) *status = 1;
 }
 
-struct RowsArgs {
-  const double* M;
-  double* A;
-  uint64_t lo, hi;
-  int R, ld, ldp, T;
-  uint64_t ntiles;
-  const double* L;
-  const int* status;
-  double* part;  // gridDim.x x stats_len(R)
-  bool solve, inner;
-};
+// ---------------------------------------------------------------- row solves
+// Per row m (length R): forward L y = m, back L^T x = y — the oracle's substitution
+// order (C-7, ascending k in both sums); the pivots are applied as reciprocals.
+// inner = y . y = m . x (the row's share of <X, Z>).
+// One thread per row; the rows of a CTA sit in a shared-memory tile with stride ld+2
+// (= 2 mod 4 doubles: conflict-free 128-bit accesses), L is staged once per CTA and
+// read with warp-broadcast loads; the forward sums read (x, L) pairs with 128-bit loads.
+__global__ void __launch_bounds__(128) solve_kernel(const double* __restrict__ M,
+                                                    double* __restrict__ A, uint64_t lo,
+                                                    uint64_t hi, int R, int ld,
+                                                    const double* __restrict__ L,
+                                                    const int* status, double* inner_part) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double red[128];
+  const int ldp = ld + 2;
+  double* Ls = sm;               // ld x ld (row stride ld, even), zero outside R x R
+  double* rinv = sm + ld * ld;   // ld
+  double* tile = rinv + ld;      // blockDim x ldp
+  const bool dead = status && *status;
+  for (int e = threadIdx.x; e < ld * ld; e += blockDim.x) {
+    const int j = e / ld, k = e % ld;
+    Ls[e] = (j < R && k < R) ? L[j * R + k] : 0.0;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < R; j += blockDim.x) rinv[j] = 1.0 / Ls[j * ld + j];
+  const uint64_t row0 = lo + blockIdx.x * (uint64_t)blockDim.x;
+  const uint64_t left = hi - row0;
+  const int nrows = left < (uint64_t)blockDim.x ? (int)left : (int)blockDim.x;
+  for (int e = threadIdx.x; e < nrows * ld; e += blockDim.x)
+    tile[(e / ld) * ldp + e % ld] = M[row0 * ld + e];
+  __syncthreads();
+  double inner = 0.0;
+  if (!dead && (int)threadIdx.x < nrows) {
+    double* x = tile + threadIdx.x * ldp;
+    for (int j = 0; j < R; ++j) {                 // L y = m
+      const double* Lj = Ls + j * ld;
+      double s = x[j];
+      int k = 0;
+#pragma unroll 4
+      for (; k + 1 < j; k += 2) {
+        const double2 xv = *reinterpret_cast<const double2*>(x + k);
+        const double2 lv = *reinterpret_cast<const double2*>(Lj + k);
+        s = fma(-lv.x, xv.x, s);
+        s = fma(-lv.y, xv.y, s);
+      }
+      if (k < j) s = fma(-Lj[k], x[k], s);
+      x[j] = s * rinv[j];
+      inner = fma(x[j], x[j], inner);
+    }
+    for (int j = R - 1; j >= 0; --j) {            // L^T x = y
+      double s = x[j];
+#pragma unroll 4
+      for (int k = j + 1; k < R; ++k) s = fma(-Ls[k * ld + j], x[k], s);
+      x[j] = s * rinv[j];
+    }
+  }
+  __syncthreads();
+  if (!dead)
+    for (int e = threadIdx.x; e < nrows * ld; e += blockDim.x) {
+      const int c = e % ld;
+      A[row0 * ld + e] = (c < R) ? tile[(e / ld) * ldp + c] : 0.0;
+    }
+  const double tot = block_sum(inner, red);
+  if (threadIdx.x == 0) inner_part[blockIdx.x] = tot;
+}
 
-// Block pair q of the upper block triangle of an nb x nb grid of 4x4 blocks.
+// ------------------------------------------------------------ Gram + colmax
+// Partial G = A^T A and colmax |A| over rows [lo, hi).  Tiles of kGT rows are staged in
+// shared memory; each thread owns a 4x4 block of the upper block triangle and a row
+// subset (rows r = s mod S), subsets are combined in shared memory at the end.
+constexpr int kGT = 64;
+constexpr int kMaxBP = 3;  // block pairs per thread when there are more than 256
+
 __device__ __forceinline__ void block_pair(int q, int nb, int& rb, int& cb) {
   int r = 0;
   while (q >= nb - r) { q -= nb - r; ++r; }
@@ -170,73 +230,45 @@ __device__ __forceinline__ void block_pair(int q, int nb, int& rb, int& cb) {
   cb = r + q;
 }
 
-constexpr int kMaxBP = 3;  // ceil(528 / 256) block pairs per thread for R <= 128
-
-__global__ void __launch_bounds__(kThreads) rows_kernel(const RowsArgs a) {
+__global__ void __launch_bounds__(kThreads) gram_kernel(const double* __restrict__ A,
+                                                        uint64_t lo, uint64_t hi, int R, int ld,
+                                                        uint64_t ntiles, double* __restrict__ part,
+                                                        const int* status) {
   extern __shared__ double sm[];
-  __shared__ double red[kThreads];
-  const int R = a.R, ld = a.ld, ldp = a.ldp;
+  const int ldp = ld + 1;
+  double* tile = sm;                          // kGT x ldp
+  double* comb = sm + kGT * ldp;              // S x nbp x 16 (S > 1 only)
   const size_t SL = (size_t)R * R + R + 1;
-  double* part = a.part + (size_t)blockIdx.x * SL;
-  if (a.status && *a.status) {
-    for (size_t e = threadIdx.x; e < SL; e += blockDim.x) part[e] = 0.0;
-    return;
-  }
-  double* Ls = sm;
-  double* tile = sm + (a.solve ? R * R : 0);
-  if (a.solve)
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) Ls[e] = a.L[e];
+  double* out = part + (size_t)blockIdx.x * SL;
   const int nb = ld / 4;
   const int nbp = nb * (nb + 1) / 2;
+  const int S = nbp >= kThreads ? 1 : kThreads / nbp;
+  const bool dead = status && *status;
   int rb[kMaxBP], cb[kMaxBP];
   double g[kMaxBP][16];
+  const int s_id = (S > 1) ? (int)threadIdx.x / nbp : 0;
 #pragma unroll
   for (int k = 0; k < kMaxBP; ++k) {
-    const int q = threadIdx.x + k * blockDim.x;
+    const int q = (S > 1) ? (int)threadIdx.x % nbp + k * nbp : (int)threadIdx.x + k * kThreads;
     rb[k] = cb[k] = -1;
-    if (q < nbp) block_pair(q, nb, rb[k], cb[k]);
+    if ((S > 1 ? (k == 0 && s_id < S) : q < nbp)) block_pair(q, nb, rb[k], cb[k]);
 #pragma unroll
     for (int z = 0; z < 16; ++z) g[k][z] = 0.0;
   }
-  double cmax = 0.0, inner = 0.0;
-  const double* src = a.solve ? a.M : a.A;
-  for (uint64_t tI = blockIdx.x; tI < a.ntiles; tI += gridDim.x) {
-    const uint64_t row0 = a.lo + tI * a.T;
-    const uint64_t left = a.hi - row0;
-    const int nrows = left < (uint64_t)a.T ? (int)left : a.T;
+  double cmax = 0.0;
+  for (uint64_t tI = blockIdx.x; tI < ntiles && !dead; tI += gridDim.x) {
+    const uint64_t row0 = lo + tI * kGT;
+    const uint64_t left = hi - row0;
+    const int nrows = left < (uint64_t)kGT ? (int)left : kGT;
     __syncthreads();
-    for (int e = threadIdx.x; e < nrows * ld; e += blockDim.x) {
-      const int r = e / ld, c = e % ld;
-      tile[r * ldp + c] = src[(row0 + r) * ld + c];
-    }
+    for (int e = threadIdx.x; e < nrows * ld; e += blockDim.x)
+      tile[(e / ld) * ldp + e % ld] = A[row0 * ld + e];
     __syncthreads();
-    if (a.solve) {
-      if ((int)threadIdx.x < nrows) {
-        double* x = tile + threadIdx.x * ldp;
-        for (int j = 0; j < R; ++j) {          // L y = m
-          double s = x[j];
-          for (int k = 0; k < j; ++k) s -= Ls[j * R + k] * x[k];
-          x[j] = s / Ls[j * R + j];
-        }
-        for (int j = R - 1; j >= 0; --j) {     // L^T x = y
-          double s = x[j];
-          for (int k = j + 1; k < R; ++k) s -= Ls[k * R + j] * x[k];
-          x[j] = s / Ls[j * R + j];
-        }
-      }
-      __syncthreads();
-      for (int e = threadIdx.x; e < nrows * ld; e += blockDim.x) {
-        const int r = e / ld, c = e % ld;
-        const double x = (c < R) ? tile[r * ldp + c] : 0.0;
-        a.A[(row0 + r) * ld + c] = x;
-        if (a.inner && c < R) inner = fma(a.M[(row0 + r) * ld + c], x, inner);
-      }
-    }
 #pragma unroll
     for (int k = 0; k < kMaxBP; ++k) {
       if (rb[k] < 0) continue;
       const int c0 = 4 * rb[k], c1 = 4 * cb[k];
-      for (int r = 0; r < nrows; ++r) {
+      for (int r = s_id; r < nrows; r += S) {
         const double* row = tile + r * ldp;
         double u[4], w[4];
 #pragma unroll
@@ -250,7 +282,21 @@ __global__ void __launch_bounds__(kThreads) rows_kernel(const RowsArgs a) {
     if ((int)threadIdx.x < R)
       for (int r = 0; r < nrows; ++r) cmax = fmax(cmax, fabs(tile[r * ldp + threadIdx.x]));
   }
-  // Per-CTA partials: symmetric Gram, colmax, inner.
+  if (S > 1) {
+    __syncthreads();
+    if (rb[0] >= 0)
+      for (int z = 0; z < 16; ++z) comb[((size_t)s_id * nbp + threadIdx.x % nbp) * 16 + z] = g[0][z];
+    __syncthreads();
+    if ((int)threadIdx.x < nbp) {
+      for (int z = 0; z < 16; ++z) {
+        double acc = 0.0;
+        for (int s = 0; s < S; ++s) acc += comb[((size_t)s * nbp + threadIdx.x) * 16 + z];
+        g[0][z] = acc;
+      }
+    } else {
+      rb[0] = -1;
+    }
+  }
 #pragma unroll
   for (int k = 0; k < kMaxBP; ++k) {
     if (rb[k] < 0) continue;
@@ -258,28 +304,42 @@ __global__ void __launch_bounds__(kThreads) rows_kernel(const RowsArgs a) {
       for (int j = 0; j < 4; ++j) {
         const int r = 4 * rb[k] + i, s = 4 * cb[k] + j;
         if (r < R && s < R && r <= s) {
-          part[(size_t)r * R + s] = g[k][i * 4 + j];
-          part[(size_t)s * R + r] = g[k][i * 4 + j];
+          out[(size_t)r * R + s] = g[k][i * 4 + j];
+          out[(size_t)s * R + r] = g[k][i * 4 + j];
         }
       }
   }
-  if ((int)threadIdx.x < R) part[(size_t)R * R + 1 + threadIdx.x] = cmax;
-  const double tot = block_sum(inner, red);
-  if (threadIdx.x == 0) part[(size_t)R * R] = tot;
+  if (threadIdx.x == 0) out[(size_t)R * R] = 0.0;
+  if ((int)threadIdx.x < R) out[(size_t)R * R + 1 + threadIdx.x] = cmax;
 }
 
+// stats[e] = fixed-order reduction over P partials: one warp per element, lane l sums
+// partials l, l+32, ... then a fixed shuffle tree.  Element R*R (inner) sums the solve
+// kernel's per-CTA inner partials instead.
 __global__ void reduce_stats_kernel(const double* __restrict__ part, int P, int R,
+                                    const double* __restrict__ inner_part, int PI,
                                     double* __restrict__ out) {
   const size_t SL = (size_t)R * R + R + 1;
-  const size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const size_t e = blockIdx.x * (size_t)(blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
   if (e >= SL) return;
   const bool is_max = e > (size_t)R * R;
+  const bool is_inner = e == (size_t)R * R;
   double acc = 0.0;
-  for (int p = 0; p < P; ++p) {
-    const double v = part[(size_t)p * SL + e];
+  if (is_inner) {
+    for (int p = lane; p < PI; p += 32) acc += inner_part[p];
+  } else {
+    for (int p = lane; p < P; p += 32) {
+      const double v = part[(size_t)p * SL + e];
+      acc = is_max ? fmax(acc, v) : acc + v;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const double v = __shfl_down_sync(0xffffffffu, acc, o);
     acc = is_max ? fmax(acc, v) : acc + v;
   }
-  out[e] = acc;
+  if (lane == 0) out[e] = acc;
 }
 
 __global__ void lambda_gram_kernel(const double* __restrict__ st, int R, int first,
@@ -356,6 +416,23 @@ int grid_stride_blocks(splatt_ctx* ctx, uint64_t n) {
                                                        (uint64_t)ctx->num_sms * 8));
 }
 
+// Returns the number of CTAs (= inner partials written).
+int launch_solve(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, uint64_t hi, int R,
+                 int ld, const double* L, const int* status, double* inner_part) {
+  const int bd = ld > 96 ? 64 : 128;  // rows per CTA; L + tile stay under 200 KB
+  const size_t smem = ((size_t)ld * ld + ld + bd * (size_t)(ld + 2)) * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    SB_CUDA(cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024));
+    attr_set = true;
+  }
+  const int nblk = (int)ceil_div(hi - lo, bd);
+  solve_kernel<<<nblk, bd, smem, ctx->stream>>>(M, A, lo, hi, R, ld, L, status, inner_part);
+  SB_CHECK_LAUNCH(ctx);
+  return nblk;
+}
+
 }  // namespace
 
 void init_factor(splatt_ctx* ctx, double* A, uint64_t I, int R, int ld, uint64_t seed,
@@ -391,45 +468,39 @@ void hadamard_cholesky(splatt_ctx* ctx, const double* G_all, int N, int n, int R
 void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, uint64_t hi,
                       int R, int ld, const double* L, bool solve, bool inner, const int* status,
                       double* stats) {
+  (void)inner;  // the inner product is always produced by the solve (it is free)
   const size_t SL = stats_len(R);
   if (hi <= lo) {
     SB_CUDA(cudaMemsetAsync(stats, 0, SL * sizeof(double), ctx->stream));
     return;
   }
-  const int ldp = ld + 1;
-  const size_t budget = 200 * 1024;
-  const size_t lbytes = solve ? (size_t)R * R * 8 : 0;
-  int T = (int)std::min<size_t>(256, (budget - lbytes) / ((size_t)ldp * 8));
-  T = std::max(32, T / 32 * 32);
-  const size_t smem = lbytes + (size_t)T * ldp * 8;
+  cudaStream_t s = ctx->stream;
+  // 1. row solves (+ per-CTA fit inner products)
+  DevBuf<double> ipart(solve ? ceil_div(hi - lo, 64) : 1, s);
+  int sblocks = 1;
+  if (solve) {
+    sblocks = launch_solve(ctx, M, A, lo, hi, R, ld, L, status, ipart.p);
+  } else {
+    SB_CUDA(cudaMemsetAsync(ipart.p, 0, sizeof(double), s));
+  }
+  // 2. partial Gram + colmax of the solved rows
+  const uint64_t ntiles = ceil_div(hi - lo, kGT);
+  const int nb = ld / 4, nbp = nb * (nb + 1) / 2;
+  const int S = nbp >= kThreads ? 1 : kThreads / nbp;
+  const size_t smem = ((size_t)kGT * (ld + 1) + (S > 1 ? (size_t)S * nbp * 16 : 0)) * 8;
   static bool attr_set = false;
   if (!attr_set) {
-    SB_CUDA(cudaFuncSetAttribute(rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(budget + 8 * 1024)));
+    SB_CUDA(cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 160 * 1024));
     attr_set = true;
   }
-  RowsArgs a{};
-  a.M = M;
-  a.A = A;
-  a.lo = lo;
-  a.hi = hi;
-  a.R = R;
-  a.ld = ld;
-  a.ldp = ldp;
-  a.T = T;
-  a.ntiles = ceil_div(hi - lo, T);
-  a.L = L;
-  a.status = status;
-  a.solve = solve;
-  a.inner = inner;
-  const int per_sm = std::max<int>(1, (int)((228 * 1024) / (smem + 2048)));
-  const int P = (int)std::min<uint64_t>(a.ntiles, (uint64_t)ctx->num_sms * std::min(per_sm, 2));
-  DevBuf<double> part((size_t)P * SL, ctx->stream);
-  a.part = part.p;
-  rows_kernel<<<P, kThreads, smem, ctx->stream>>>(a);
+  const int P = (int)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * 2);
+  DevBuf<double> part((size_t)P * SL, s);
+  gram_kernel<<<P, kThreads, smem, s>>>(A, lo, hi, R, ld, ntiles, part.p, status);
   SB_CHECK_LAUNCH(ctx);
-  reduce_stats_kernel<<<(unsigned)ceil_div(SL, kThreads), kThreads, 0, ctx->stream>>>(part.p, P, R,
-                                                                                     stats);
+  // 3. fixed-order reduction
+  reduce_stats_kernel<<<(unsigned)ceil_div(SL, kThreads / 32), kThreads, 0, s>>>(
+      part.p, P, R, ipart.p, solve ? sblocks : 1, stats);
   SB_CHECK_LAUNCH(ctx);
 }
 
