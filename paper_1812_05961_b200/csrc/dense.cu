@@ -5,11 +5,10 @@
 // (line 6), Gram refresh, and the fit (line 13).  Readings: DESIGN.md §2 (C-7 pivot
 // threshold / ridge, C-8 norm schedule, C-10 fit identity).
 //
-// Structure: one CTA factors V; the row solves run one row per thread
-// on a shared-memory tile and also return the fit inner
-// product <M_i, A_i> = |L^-1 M_i|^2 of every row; one pass over the solved rows gives
-// the partial Gram and column max |a|; partials are reduced in a fixed order, so every
-// result is deterministic.
+// Structure: one CTA factors V (right-looking Cholesky); persistent CTAs
+// solve tiles of rows in shared memory and, while a solved tile is still on chip, add
+// its partial Gram, column max |a| and fit inner product <M_i, A_i> = |L^-1 M_i|^2;
+// partials are reduced in a fixed order, so every result is deterministic.
 #include <algorithm>
 #include <cmath>
 
@@ -123,23 +122,25 @@ __global__ void hadamard_cholesky_kernel(const double* __restrict__ G_all, int N
       thr = 1e-12 * mx;
     }
     __syncthreads();
+    // Right-looking: after step j, W[i][k] (k > j, i >= k) holds V[i][k] - sum_{m<=j}
+    // L[i][m] L[k][m], accumulated in ascending m — the same sums, in the same order, as
+    // the oracle's Cholesky-Banachiewicz; every step is one parallel pass.
     for (int j = 0; j < R; ++j) {
-      if (threadIdx.x == 0) {
-        double d = W[j * R + j];
-        for (int k = 0; k < j; ++k) d -= W[j * R + k] * W[j * R + k];
-        if (d > thr) W[j * R + j] = sqrt(d);
-        else failed = 1;
-      }
+      const double d = W[j * R + j];
+      if (!(d > thr)) { failed = 1; break; }   // uniform: every thread reads the same d
+      const double piv = sqrt(d);
       __syncthreads();
-      if (failed) break;
-      const double piv = W[j * R + j];
-      for (int i = j + 1 + threadIdx.x; i < R; i += blockDim.x) {
-        double s = W[i * R + j];
-        for (int k = 0; k < j; ++k) s -= W[i * R + k] * W[j * R + k];
-        W[i * R + j] = s / piv;
+      if (threadIdx.x == 0) W[j * R + j] = piv;
+      for (int i = j + 1 + threadIdx.x; i < R; i += blockDim.x) W[i * R + j] = W[i * R + j] / piv;
+      __syncthreads();
+      const int m = R - 1 - j;  // trailing size
+      for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+        const int i = j + 1 + e / m, k = j + 1 + e % m;
+        if (k <= i) W[i * R + k] -= W[i * R + j] * W[k * R + j];
       }
       __syncthreads();
     }
+    __syncthreads();
     if (!failed) {
       for (int e = threadIdx.x; e < RR; e += blockDim.x)
         L[e] = (e % R <= e / R) ? W[e] : 0.0;
@@ -150,79 +151,15 @@ __global__ void hadamard_cholesky_kernel(const double* __restrict__ G_all, int N
   if (threadIdx.x == 0) *status = 1;
 }
 
-// ---------------------------------------------------------------- row solves
-// Per row m (length R): forward L y = m, back L^T x = y — the oracle's substitution
-// order (C-7, ascending k in both sums); the pivots are applied as reciprocals.
-// inner = y . y = m . x (the row's share of <X, Z>).
-// One thread per row; the rows of a CTA sit in a shared-memory tile with stride ld+2
-// (= 2 mod 4 doubles: conflict-free 128-bit accesses), L is staged once per CTA and
-// read with warp-broadcast loads; the forward sums read (x, L) pairs with 128-bit loads.
-__global__ void __launch_bounds__(128) solve_kernel(const double* __restrict__ M,
-                                                    double* __restrict__ A, uint64_t lo,
-                                                    uint64_t hi, int R, int ld,
-                                                    const double* __restrict__ L,
-                                                    const int* status, double* inner_part) {
-  extern __shared__ __align__(16) double sm[];
-  __shared__ double red[128];
-  const int ldp = ld + 2;
-  double* Ls = sm;               // ld x ld (row stride ld, even), zero outside R x R
-  double* rinv = sm + ld * ld;   // ld
-  double* tile = rinv + ld;      // blockDim x ldp
-  const bool dead = status && *status;
-  for (int e = threadIdx.x; e < ld * ld; e += blockDim.x) {
-    const int j = e / ld, k = e % ld;
-    Ls[e] = (j < R && k < R) ? L[j * R + k] : 0.0;
-  }
-  __syncthreads();
-  for (int j = threadIdx.x; j < R; j += blockDim.x) rinv[j] = 1.0 / Ls[j * ld + j];
-  const uint64_t row0 = lo + blockIdx.x * (uint64_t)blockDim.x;
-  const uint64_t left = hi - row0;
-  const int nrows = left < (uint64_t)blockDim.x ? (int)left : (int)blockDim.x;
-  for (int e = threadIdx.x; e < nrows * ld; e += blockDim.x)
-    tile[(e / ld) * ldp + e % ld] = M[row0 * ld + e];
-  __syncthreads();
-  double inner = 0.0;
-  if (!dead && (int)threadIdx.x < nrows) {
-    double* x = tile + threadIdx.x * ldp;
-    for (int j = 0; j < R; ++j) {                 // L y = m
-      const double* Lj = Ls + j * ld;
-      double s = x[j];
-      int k = 0;
-#pragma unroll 4
-      for (; k + 1 < j; k += 2) {
-        const double2 xv = *reinterpret_cast<const double2*>(x + k);
-        const double2 lv = *reinterpret_cast<const double2*>(Lj + k);
-        s = fma(-lv.x, xv.x, s);
-        s = fma(-lv.y, xv.y, s);
-      }
-      if (k < j) s = fma(-Lj[k], x[k], s);
-      x[j] = s * rinv[j];
-      inner = fma(x[j], x[j], inner);
-    }
-    for (int j = R - 1; j >= 0; --j) {            // L^T x = y
-      double s = x[j];
-#pragma unroll 4
-      for (int k = j + 1; k < R; ++k) s = fma(-Ls[k * ld + j], x[k], s);
-      x[j] = s * rinv[j];
-    }
-  }
-  __syncthreads();
-  if (!dead)
-    for (int e = threadIdx.x; e < nrows * ld; e += blockDim.x) {
-      const int c = e % ld;
-      A[row0 * ld + e] = (c < R) ? tile[(e / ld) * ldp + c] : 0.0;
-    }
-  const double tot = block_sum(inner, red);
-  if (threadIdx.x == 0) inner_part[blockIdx.x] = tot;
-}
-
-// ------------------------------------------------------------ Gram + colmax
-// Partial G = A^T A and colmax |A| over rows [lo, hi).  Tiles of kGT rows are staged in
-// shared memory; each thread owns a 4x4 block of the upper block triangle and a row
-// subset (rows r = s mod S), subsets are combined in shared memory at the end.
-constexpr int kGT = 64;
-constexpr int kMaxBP = 3;  // block pairs per thread when there are more than 256
-
+// ------------------------------------------------- row solves + Gram + colmax
+// Per row m (length R): forward L y = m, back L^T x = y (C-7; the pivots are applied
+// as reciprocals, the sums split over two accumulators).  inner = y . y = m . x, the
+// row's share of <X, Z> (C-10).  Persistent CTAs walk tiles of T rows staged in shared
+// memory (stride ld+2 = 2 mod 4 doubles: conflict-free 128-bit accesses): one thread
+// solves one row, the solved tile is written back coalesced, and while it is still in
+// shared memory every thread accumulates a 4x4 block of the partial Gram (rows split
+// into S subsets when there are fewer block pairs than threads) and the column max |a|.
+// Without `solve` the kernel only reads A (initial Grams).
 __device__ __forceinline__ void block_pair(int q, int nb, int& rb, int& cb) {
   int r = 0;
   while (q >= nb - r) { q -= nb - r; ++r; }
@@ -230,23 +167,42 @@ __device__ __forceinline__ void block_pair(int q, int nb, int& rb, int& cb) {
   cb = r + q;
 }
 
-__global__ void __launch_bounds__(kThreads) gram_kernel(const double* __restrict__ A,
-                                                        uint64_t lo, uint64_t hi, int R, int ld,
-                                                        uint64_t ntiles, double* __restrict__ part,
-                                                        const int* status) {
-  extern __shared__ double sm[];
-  const int ldp = ld + 1;
-  double* tile = sm;                          // kGT x ldp
-  double* comb = sm + kGT * ldp;              // S x nbp x 16 (S > 1 only)
+struct RowsArgs {
+  const double* M;
+  double* A;
+  uint64_t lo, hi, ntiles;
+  int R, ld, T;
+  const double* L;
+  const int* status;
+  double* part;  // gridDim.x x stats_len(R)
+  bool solve;
+};
+
+template <int kMaxBP>  // 1 when there are <= 256 block pairs (ld <= 88), else 3
+__global__ void __launch_bounds__(kThreads) solve_gram_kernel(const RowsArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double red[kThreads];
+  const int R = a.R, ld = a.ld, ldp = ld + 2, T = a.T;
   const size_t SL = (size_t)R * R + R + 1;
-  double* out = part + (size_t)blockIdx.x * SL;
+  double* out = a.part + (size_t)blockIdx.x * SL;
+  double* Ls = sm;                                   // ld x ld if solve
+  double* rinv = Ls + (a.solve ? ld * ld : 0);       // ld
+  double* tile = rinv + ld;                          // T x ldp
+  const bool dead = a.status && *a.status;
+  if (a.solve) {
+    for (int e = threadIdx.x; e < ld * ld; e += blockDim.x) {
+      const int j = e / ld, k = e % ld;
+      Ls[e] = (j < R && k < R) ? a.L[j * R + k] : 0.0;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < R; j += blockDim.x) rinv[j] = 1.0 / Ls[j * ld + j];
+  }
   const int nb = ld / 4;
   const int nbp = nb * (nb + 1) / 2;
   const int S = nbp >= kThreads ? 1 : kThreads / nbp;
-  const bool dead = status && *status;
+  const int s_id = (S > 1) ? (int)threadIdx.x / nbp : 0;
   int rb[kMaxBP], cb[kMaxBP];
   double g[kMaxBP][16];
-  const int s_id = (S > 1) ? (int)threadIdx.x / nbp : 0;
 #pragma unroll
   for (int k = 0; k < kMaxBP; ++k) {
     const int q = (S > 1) ? (int)threadIdx.x % nbp + k * nbp : (int)threadIdx.x + k * kThreads;
@@ -255,24 +211,74 @@ __global__ void __launch_bounds__(kThreads) gram_kernel(const double* __restrict
 #pragma unroll
     for (int z = 0; z < 16; ++z) g[k][z] = 0.0;
   }
-  double cmax = 0.0;
-  for (uint64_t tI = blockIdx.x; tI < ntiles && !dead; tI += gridDim.x) {
-    const uint64_t row0 = lo + tI * kGT;
-    const uint64_t left = hi - row0;
-    const int nrows = left < (uint64_t)kGT ? (int)left : kGT;
+  double cmax = 0.0, inner = 0.0;
+  const double* src = a.solve ? a.M : a.A;
+  for (uint64_t tI = blockIdx.x; tI < a.ntiles && !dead; tI += gridDim.x) {
+    const uint64_t row0 = a.lo + tI * T;
+    const uint64_t left = a.hi - row0;
+    const int nrows = left < (uint64_t)T ? (int)left : T;
     __syncthreads();
-    for (int e = threadIdx.x; e < nrows * ld; e += blockDim.x)
-      tile[(e / ld) * ldp + e % ld] = A[row0 * ld + e];
+    {  // async 16-byte copies global -> padded tile (no register staging, all in flight)
+      const int half = ld / 2;  // 16-byte pairs per row
+      const double* g = src + row0 * ld;
+      for (int e = threadIdx.x; e < nrows * half; e += blockDim.x) {
+        const int r = e / half, c = 2 * (e % half);
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(tile + r * ldp + c);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(g + 2 * e));
+      }
+      asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    }
     __syncthreads();
+    if (a.solve) {
+      for (int t = threadIdx.x; t < nrows; t += blockDim.x) {
+        double* x = tile + t * ldp;
+        for (int j = 0; j < R; ++j) {                 // L y = m
+          const double* Lj = Ls + j * ld;
+          double s0 = x[j], s1 = 0.0;
+          int k = 0;
+#pragma unroll 4
+          for (; k + 1 < j; k += 2) {
+            const double2 xv = *reinterpret_cast<const double2*>(x + k);
+            const double2 lv = *reinterpret_cast<const double2*>(Lj + k);
+            s0 = fma(-lv.x, xv.x, s0);
+            s1 = fma(-lv.y, xv.y, s1);
+          }
+          if (k < j) s0 = fma(-Lj[k], x[k], s0);
+          const double y = (s0 + s1) * rinv[j];
+          x[j] = y;
+          inner = fma(y, y, inner);
+        }
+        for (int j = R - 1; j >= 0; --j) {            // L^T x = y
+          double s0 = x[j], s1 = 0.0;
+          int k = j + 1;
+#pragma unroll 4
+          for (; k + 1 < R; k += 2) {
+            s0 = fma(-Ls[k * ld + j], x[k], s0);
+            s1 = fma(-Ls[(k + 1) * ld + j], x[k + 1], s1);
+          }
+          if (k < R) s0 = fma(-Ls[k * ld + j], x[k], s0);
+          x[j] = (s0 + s1) * rinv[j];
+        }
+        for (int j = R; j < ld; ++j) x[j] = 0.0;
+      }
+      __syncthreads();
+      const int half = ld / 2;
+      double2* dst = reinterpret_cast<double2*>(a.A + row0 * ld);
+      for (int e = threadIdx.x; e < nrows * half; e += blockDim.x)
+        dst[e] = *reinterpret_cast<const double2*>(tile + (e / half) * ldp + 2 * (e % half));
+    }
 #pragma unroll
     for (int k = 0; k < kMaxBP; ++k) {
       if (rb[k] < 0) continue;
       const int c0 = 4 * rb[k], c1 = 4 * cb[k];
       for (int r = s_id; r < nrows; r += S) {
         const double* row = tile + r * ldp;
-        double u[4], w[4];
-#pragma unroll
-        for (int z = 0; z < 4; ++z) { u[z] = row[c0 + z]; w[z] = row[c1 + z]; }
+        const double2 u01 = *reinterpret_cast<const double2*>(row + c0);
+        const double2 u23 = *reinterpret_cast<const double2*>(row + c0 + 2);
+        const double2 w01 = *reinterpret_cast<const double2*>(row + c1);
+        const double2 w23 = *reinterpret_cast<const double2*>(row + c1 + 2);
+        const double u[4] = {u01.x, u01.y, u23.x, u23.y};
+        const double w[4] = {w01.x, w01.y, w23.x, w23.y};
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -282,7 +288,8 @@ __global__ void __launch_bounds__(kThreads) gram_kernel(const double* __restrict
     if ((int)threadIdx.x < R)
       for (int r = 0; r < nrows; ++r) cmax = fmax(cmax, fabs(tile[r * ldp + threadIdx.x]));
   }
-  if (S > 1) {
+  if (S > 1) {  // combine the row subsets (reuses the tile area)
+    double* comb = tile;
     __syncthreads();
     if (rb[0] >= 0)
       for (int z = 0; z < 16; ++z) comb[((size_t)s_id * nbp + threadIdx.x % nbp) * 16 + z] = g[0][z];
@@ -309,30 +316,24 @@ __global__ void __launch_bounds__(kThreads) gram_kernel(const double* __restrict
         }
       }
   }
-  if (threadIdx.x == 0) out[(size_t)R * R] = 0.0;
   if ((int)threadIdx.x < R) out[(size_t)R * R + 1 + threadIdx.x] = cmax;
+  const double tot = block_sum(inner, red);
+  if (threadIdx.x == 0) out[(size_t)R * R] = tot;
 }
 
 // stats[e] = fixed-order reduction over P partials: one warp per element, lane l sums
-// partials l, l+32, ... then a fixed shuffle tree.  Element R*R (inner) sums the solve
-// kernel's per-CTA inner partials instead.
+// partials l, l+32, ... then a fixed shuffle tree (sum; max for the colmax entries).
 __global__ void reduce_stats_kernel(const double* __restrict__ part, int P, int R,
-                                    const double* __restrict__ inner_part, int PI,
                                     double* __restrict__ out) {
   const size_t SL = (size_t)R * R + R + 1;
   const size_t e = blockIdx.x * (size_t)(blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (e >= SL) return;
   const bool is_max = e > (size_t)R * R;
-  const bool is_inner = e == (size_t)R * R;
   double acc = 0.0;
-  if (is_inner) {
-    for (int p = lane; p < PI; p += 32) acc += inner_part[p];
-  } else {
-    for (int p = lane; p < P; p += 32) {
-      const double v = part[(size_t)p * SL + e];
-      acc = is_max ? fmax(acc, v) : acc + v;
-    }
+  for (int p = lane; p < P; p += 32) {
+    const double v = part[(size_t)p * SL + e];
+    acc = is_max ? fmax(acc, v) : acc + v;
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
@@ -416,23 +417,6 @@ int grid_stride_blocks(splatt_ctx* ctx, uint64_t n) {
                                                        (uint64_t)ctx->num_sms * 8));
 }
 
-// Returns the number of CTAs (= inner partials written).
-int launch_solve(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, uint64_t hi, int R,
-                 int ld, const double* L, const int* status, double* inner_part) {
-  const int bd = ld > 96 ? 64 : 128;  // rows per CTA; L + tile stay under 200 KB
-  const size_t smem = ((size_t)ld * ld + ld + bd * (size_t)(ld + 2)) * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
-    SB_CUDA(cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 200 * 1024));
-    attr_set = true;
-  }
-  const int nblk = (int)ceil_div(hi - lo, bd);
-  solve_kernel<<<nblk, bd, smem, ctx->stream>>>(M, A, lo, hi, R, ld, L, status, inner_part);
-  SB_CHECK_LAUNCH(ctx);
-  return nblk;
-}
-
 }  // namespace
 
 void init_factor(splatt_ctx* ctx, double* A, uint64_t I, int R, int ld, uint64_t seed,
@@ -470,37 +454,50 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
                       double* stats) {
   (void)inner;  // the inner product is always produced by the solve (it is free)
   const size_t SL = stats_len(R);
+  cudaStream_t s = ctx->stream;
   if (hi <= lo) {
-    SB_CUDA(cudaMemsetAsync(stats, 0, SL * sizeof(double), ctx->stream));
+    SB_CUDA(cudaMemsetAsync(stats, 0, SL * sizeof(double), s));
     return;
   }
-  cudaStream_t s = ctx->stream;
-  // 1. row solves (+ per-CTA fit inner products)
-  DevBuf<double> ipart(solve ? ceil_div(hi - lo, 64) : 1, s);
-  int sblocks = 1;
-  if (solve) {
-    sblocks = launch_solve(ctx, M, A, lo, hi, R, ld, L, status, ipart.p);
-  } else {
-    SB_CUDA(cudaMemsetAsync(ipart.p, 0, sizeof(double), s));
-  }
-  // 2. partial Gram + colmax of the solved rows
-  const uint64_t ntiles = ceil_div(hi - lo, kGT);
+  const int ldp = ld + 2;
+  const size_t budget = 190 * 1024;
+  const size_t lbytes = solve ? (size_t)ld * ld * 8 : 0;
   const int nb = ld / 4, nbp = nb * (nb + 1) / 2;
   const int S = nbp >= kThreads ? 1 : kThreads / nbp;
-  const size_t smem = ((size_t)kGT * (ld + 1) + (S > 1 ? (size_t)S * nbp * 16 : 0)) * 8;
+  int T = (int)std::min<size_t>(256, (budget - lbytes - (size_t)ld * 8) / ((size_t)ldp * 8));
+  T = std::max(32, T / 32 * 32);
+  // the subset-combine buffer aliases the tile
+  while ((size_t)T * ldp < (size_t)S * nbp * 16) T += 32;
+  const size_t smem = lbytes + (size_t)ld * 8 + (size_t)T * ldp * 8;
   static bool attr_set = false;
   if (!attr_set) {
-    SB_CUDA(cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 160 * 1024));
+    SB_CUDA(cudaFuncSetAttribute(solve_gram_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 210 * 1024));
+    SB_CUDA(cudaFuncSetAttribute(solve_gram_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 210 * 1024));
     attr_set = true;
   }
-  const int P = (int)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * 2);
+  RowsArgs a{};
+  a.M = M;
+  a.A = A;
+  a.lo = lo;
+  a.hi = hi;
+  a.R = R;
+  a.ld = ld;
+  a.T = T;
+  a.ntiles = ceil_div(hi - lo, T);
+  a.L = L;
+  a.status = status;
+  a.solve = solve;
+  const int per_sm = std::max<int>(1, (int)((228 * 1024) / (smem + 4096)));
+  const int P = (int)std::min<uint64_t>(a.ntiles, (uint64_t)ctx->num_sms * std::min(per_sm, 2));
   DevBuf<double> part((size_t)P * SL, s);
-  gram_kernel<<<P, kThreads, smem, s>>>(A, lo, hi, R, ld, ntiles, part.p, status);
+  a.part = part.p;
+  if (nbp <= kThreads) solve_gram_kernel<1><<<P, kThreads, smem, s>>>(a);
+  else solve_gram_kernel<3><<<P, kThreads, smem, s>>>(a);
   SB_CHECK_LAUNCH(ctx);
-  // 3. fixed-order reduction
-  reduce_stats_kernel<<<(unsigned)ceil_div(SL, kThreads / 32), kThreads, 0, s>>>(
-      part.p, P, R, ipart.p, solve ? sblocks : 1, stats);
+  reduce_stats_kernel<<<(unsigned)ceil_div(SL, kThreads / 32), kThreads, 0, s>>>(part.p, P, R,
+                                                                                stats);
   SB_CHECK_LAUNCH(ctx);
 }
 
