@@ -220,6 +220,8 @@ def _make_coo(ind, vals, dims):
 
 def _as_u32(a):
     if isinstance(a, np.ndarray):
+        if a.dtype == np.int32 and a.flags.c_contiguous:
+            return a.view(np.uint32)  # same bits, no copy (keeps pinned buffers pinned)
         return np.ascontiguousarray(a, dtype=np.uint32)
     import torch
     if a.dtype == torch.int32 or a.dtype == torch.uint32:
@@ -311,7 +313,8 @@ def mttkrp(csf: Csf, mode: int, factors, out=None, rank: int | None = None):
 
 
 def cpd_als(ind, vals, dims, rank: int, max_iters: int, tol: float = 0.0, seed: int = 0,
-            init=None, ctx: Context | None = None, out_device: bool = True, stats: bool = False):
+            init=None, ctx: Context | None = None, out_device: bool = True, stats: bool = False,
+            out=None):
     """splatt_cpd_als(_ex).  Returns dict(factors, lam, fit, iters, fit_history[, stats]).
 
     ind/vals may be host (numpy / CPU tensors) or CUDA tensors; outputs are CUDA
@@ -323,7 +326,12 @@ def cpd_als(ind, vals, dims, rank: int, max_iters: int, tol: float = 0.0, seed: 
     vals = _as_f64(vals.numpy() if hasattr(vals, "is_cuda") and not vals.is_cuda else vals)
     coo = _make_coo(ind, vals, dims)
     N = len(dims)
-    if out_device:
+    if out is not None:  # caller buffers (host — e.g. pinned — or device), ld = rank
+        fac, lam = list(out["factors"]), out["lam"]
+        for f, d in zip(fac, dims):
+            if tuple(f.shape) != (int(d), rank):
+                raise ValueError("out factor shape must be (I_n, rank)")
+    elif out_device:
         fac = [torch.empty((int(d), rank), dtype=torch.float64, device=f"cuda:{ctx.device}")
                for d in dims]
         lam = torch.empty(rank, dtype=torch.float64, device=f"cuda:{ctx.device}")

@@ -1,5 +1,7 @@
 // abi.cu — the extern "C" boundary (include/splatt_b200.h).  Argument checks, host<->
 // device staging, status mapping.  No arithmetic of the method happens here.
+#include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -84,6 +86,15 @@ struct StagedCoo {
       SB_CUDA(cudaMemcpyAsync(vals.p, coo->vals, coo->nnz * 8, cudaMemcpyHostToDevice,
                               ctx->stream));
       view.vals = vals.p;
+    }
+    if (getenv("SPLATT_DEBUG_STAGING")) {
+      cudaPointerAttributes at;
+      cudaPointerGetAttributes(&at, coo->vals);
+      auto t0 = std::chrono::steady_clock::now();
+      cudaStreamSynchronize(ctx->stream);
+      auto t1 = std::chrono::steady_clock::now();
+      fprintf(stderr, "[splatt] staging: vals memtype=%d, sync after enqueue %.3f ms\n",
+              (int)at.type, std::chrono::duration<double, std::milli>(t1 - t0).count());
     }
   }
 };
