@@ -60,6 +60,7 @@ enum { SPLATT_CSF_ALL = 0 };
 
 typedef struct splatt_ctx splatt_ctx;   /* device, stream, allocator pool, optional comm */
 typedef struct splatt_csf splatt_csf;   /* device-resident CSF set, immutable after build */
+typedef struct splatt_loopback splatt_loopback; /* in-process group of logical ranks     */
 
 /* Sparse tensor in coordinate form (SoA).  nmodes in [3, 8]; nnz >= 1;
  * dims[m] in [1, 2^32); ind[m][p] < dims[m]; duplicates are kept as distinct
@@ -125,6 +126,16 @@ const char*   splatt_version(void);
  * (libnccl.so.2); failure -> SPLATT_ERR_NCCL.                                      */
 splatt_status splatt_comm_unique_id(void* id128);
 splatt_status splatt_ctx_set_comm(splatt_ctx* ctx, const void* id128, int nranks, int rank);
+
+/* In-process loopback group (testing/emulation of the sharded path on ONE device): nranks
+ * logical ranks, each a host thread with its own context and its own stream (a context
+ * on the legacy default stream is rejected), run the same multi-rank ALS as above; the
+ * exchanges go through device memory with host barriers between them (no kernel waits on
+ * another rank).  nranks in [1, 8].  Destroy the group after every rank has finished.    */
+splatt_status splatt_loopback_create(int32_t nranks, splatt_loopback** out);
+splatt_status splatt_ctx_set_comm_loopback(splatt_ctx* ctx, splatt_loopback* group,
+                                           int32_t rank);
+void          splatt_loopback_destroy(splatt_loopback* group);
 
 /* Host-only (no device needed): cut S slices with nnz weights w[0..S) into G
  * contiguous ranges minimising the maximum range weight;

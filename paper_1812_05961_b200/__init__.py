@@ -19,7 +19,7 @@ import threading
 
 import numpy as np
 
-__all__ = ["lib", "Context", "Csf", "csf_build", "mttkrp", "cpd_als", "partition",
+__all__ = ["lib", "Context", "Loopback", "Csf", "csf_build", "mttkrp", "cpd_als", "partition",
            "SplattError", "SingularError", "EmptyTensorError", "STATUS", "padded_ld"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -99,6 +99,9 @@ def lib():
                 "splatt_last_error": (C.c_char_p, [P]),
                 "splatt_comm_unique_id": (st, [P]),
                 "splatt_ctx_set_comm": (st, [P, P, C.c_int, C.c_int]),
+                "splatt_loopback_create": (st, [i32, C.POINTER(P)]),
+                "splatt_ctx_set_comm_loopback": (st, [P, P, i32]),
+                "splatt_loopback_destroy": (None, [P]),
                 "splatt_partition": (st, [P, u64, i32, P]),
                 "splatt_csf_build": (st, [P, C.POINTER(Coo), i32, P, i32, C.POINTER(P)]),
                 "splatt_csf_info": (st, [P, i32, C.POINTER(i32), P, P]),
@@ -179,9 +182,36 @@ class Context:
         _raise(lib().splatt_ctx_set_comm(self._p, raw, world, rank), self._p)
         self.nranks, self.rank = world, rank
 
+    def set_comm_loopback(self, group: "Loopback", rank: int):
+        """Join an in-process loopback group as logical rank `rank` (testing the sharded
+        path on one device; the context must own a non-default stream)."""
+        _raise(lib().splatt_ctx_set_comm_loopback(self._p, group._p, rank), self._p)
+        self.nranks, self.rank = group.nranks, rank
+
     def close(self):
         if getattr(self, "_p", None):
             lib().splatt_ctx_destroy(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Loopback:
+    """splatt_loopback: a group of in-process logical ranks on one device."""
+
+    def __init__(self, nranks: int):
+        p = C.c_void_p()
+        _raise(lib().splatt_loopback_create(int(nranks), C.byref(p)))
+        self._p = p
+        self.nranks = int(nranks)
+
+    def close(self):
+        if getattr(self, "_p", None):
+            lib().splatt_loopback_destroy(self._p)
             self._p = None
 
     def __del__(self):

@@ -23,6 +23,7 @@ struct Comm {
 };
 
 std::unique_ptr<Comm> make_nccl_comm(const void* id128, int nranks, int rank);
+std::unique_ptr<Comm> make_loopback_comm(splatt_loopback* group, int rank);
 
 }  // namespace sb
 

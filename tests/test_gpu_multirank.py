@@ -1,0 +1,99 @@
+"""The sharded (multi-rank) CP-ALS driver on one B200 through the loopback communicator.
+
+G logical ranks (host threads, one context + stream each) run the same splatt_cpd_als as
+the NCCL ranks of a multi-GPU job: per-mode C-14 partition, local CSFs of the owned
+nonzeros, local MTTKRP + solves, all-reduce of the Gram/inner/colmax statistics and
+all-gather of the owned rows.  Every rank must return the same model,
+equal to the single-rank result up to summation order and to the oracle within 1e-7.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests.gpu_util import ALS_TOL, rel_fro
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sb(cuda_ok):
+    from paper_1812_05961_b200 import build
+    build.build()
+    import paper_1812_05961_b200 as m
+    return m
+
+
+def run_ranks(sb, t, G, R, iters, seed, tol=0.0):
+    import torch
+    grp = sb.Loopback(G)
+    results, errors = [None] * G, []
+
+    def worker(r):
+        try:
+            stream = torch.cuda.Stream(0)
+            ctx = sb.Context(0, stream=stream)
+            ctx.set_comm_loopback(grp, r)
+            with torch.cuda.stream(stream):
+                ind = [torch.from_numpy(a.view(np.int32)).cuda() for a in t.ind]
+                vals = torch.from_numpy(t.vals).cuda()
+            stream.synchronize()
+            res = sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=iters, tol=tol, seed=seed,
+                             ctx=ctx, out_device=False, stats=True)
+            results[r] = res
+            ctx.close()
+        except Exception as e:  # pragma: no cover
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(G)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(timeout=600)
+    grp.close()
+    assert not errors, errors
+    return results
+
+
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
+def test_sharded_als_matches_single_rank_and_oracle(sb, G):
+    t = synth.generate((4000, 1100, 7500), 150_000, [("zipf", 1.1)] * 3, "ratings", seed=22)
+    R, iters = 16, 5
+    single = run_ranks(sb, t, 1, R, iters, seed=5)[0]
+    multi = run_ranks(sb, t, G, R, iters, seed=5)
+    ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=R, max_iters=iters, seed=5)
+    for r in range(G):
+        assert multi[r]["stats"]["nranks"] == G
+        for n in range(3):
+            # every rank holds the identical model
+            assert np.array_equal(multi[r]["factors"][n], multi[0]["factors"][n])
+            assert rel_fro(multi[r]["factors"][n], single["factors"][n]) <= 1e-10
+            assert rel_fro(multi[r]["factors"][n], ref["factors"][n]) <= ALS_TOL
+        assert rel_fro(multi[r]["lam"], ref["lam"]) <= ALS_TOL
+        assert abs(multi[r]["fit"] - ref["fit"]) <= ALS_TOL * abs(ref["fit"])
+    # the ranks split the nonzeros of every mode (local CSF leaves sum to nnz)
+    for n in range(3):
+        assert sum(multi[r]["stats"]["csf_nodes"][n][2] for r in range(G)) == t.nnz
+
+
+def test_sharded_als_four_modes_with_empty_ranks(sb):
+    # 4-mode tensor whose last mode has fewer slices than ranks: some ranks own nothing
+    t = synth.generate((300, 200, 100, 3), 20_000, [("zipf", 1.05)] * 4, "u01", seed=9)
+    R = 8
+    multi = run_ranks(sb, t, 4, R, 3, seed=2)
+    ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=R, max_iters=3, seed=2)
+    for r in range(4):
+        for n in range(4):
+            assert rel_fro(multi[r]["factors"][n], ref["factors"][n]) <= ALS_TOL
+        assert abs(multi[r]["fit"] - ref["fit"]) <= ALS_TOL * abs(ref["fit"])
+
+
+def test_sharded_als_tol_stop(sb):
+    t = synth.generate_config("c1")
+    multi = run_ranks(sb, t, 2, 8, 100, seed=1, tol=1e-4)
+    ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=8, max_iters=100, tol=1e-4, seed=1)
+    for r in range(2):
+        assert multi[r]["iters"] == ref["iters"]
+        assert abs(multi[r]["fit"] - ref["fit"]) <= ALS_TOL * abs(ref["fit"])
