@@ -133,10 +133,11 @@ __global__ void hadamard_cholesky_kernel(const double* __restrict__ G_all, int N
       if (threadIdx.x == 0) W[j * R + j] = piv;
       for (int i = j + 1 + threadIdx.x; i < R; i += blockDim.x) W[i * R + j] = W[i * R + j] / piv;
       __syncthreads();
-      const int m = R - 1 - j;  // trailing size
-      for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-        const int i = j + 1 + e / m, k = j + 1 + e % m;
-        if (k <= i) W[i * R + k] -= W[i * R + j] * W[k * R + j];
+      // trailing update on a fixed 16 x 16 thread grid (no integer division)
+      const int ti = threadIdx.x >> 4, tk = threadIdx.x & 15;
+      for (int i = j + 1 + ti; i < R; i += 16) {
+        const double lij = W[i * R + j];
+        for (int k = j + 1 + tk; k <= i; k += 16) W[i * R + k] -= lij * W[k * R + j];
       }
       __syncthreads();
     }
