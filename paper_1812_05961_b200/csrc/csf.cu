@@ -68,6 +68,23 @@ __global__ void gather_kernel(CoordOut co, uint64_t nnz, const uint32_t* __restr
   }
 }
 
+struct BitSet { int b[SPLATT_MAX_NMODES]; };
+
+// coordinate of level l at sorted position j = bits of the sorted composite key.
+__global__ void decode_kernel(KeySpec ks, BitSet bs, CoordOut co, uint64_t nnz,
+                              const uint64_t* __restrict__ keys, const uint32_t* __restrict__ P,
+                              const double* __restrict__ vin, double* __restrict__ vout) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[j];
+    for (int l = 0; l < co.N; ++l) {
+      const uint64_t m = bs.b[l] >= 64 ? ~0ull : ((1ull << bs.b[l]) - 1ull);
+      co.dst[l][j] = (uint32_t)((k >> ks.shift[l]) & m);
+    }
+    vout[j] = vin[P[j]];
+  }
+}
+
 // node[l][j] = 1 iff a level-l node starts at sorted position j (prefix 0..l changed).
 struct FlagOut {
   const uint32_t* c[SPLATT_MAX_NMODES];
@@ -234,10 +251,11 @@ void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
     order = pout;
   }
   kA.release();
-  kB.release();
   temp.release();
 
-  // Sorted coordinates per level and the permuted values.
+  // Sorted coordinates per level and the permuted values.  With one key group the
+  // coordinates are decoded from the sorted keys (sequential reads); otherwise they are
+  // gathered through the permutation.
   DevBuf<uint32_t> coord[SPLATT_MAX_NMODES];
   CoordOut co{};
   co.N = N;
@@ -247,8 +265,24 @@ void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
     co.dst[l] = coord[l].p;
   }
   out.vals.alloc(nnz, st);
-  gather_kernel<<<grid, 256, 0, st>>>(co, nnz, order, d_vals, out.vals.p);
+  if (groups.size() == 1) {
+    KeySpec ks{};
+    int sh = 0;
+    for (int l = N - 1; l >= 0; --l) { ks.shift[l] = sh; sh += bits[l]; }
+    for (int l = 0; l < N; ++l) ks.src[l] = nullptr;
+    ks.lo = 0;
+    ks.hi = N;
+    int maskbits[SPLATT_MAX_NMODES];
+    for (int l = 0; l < N; ++l) maskbits[l] = bits[l];
+    decode_kernel<<<grid, 256, 0, st>>>(ks, BitSet{{maskbits[0], maskbits[1], maskbits[2],
+                                                    maskbits[3], maskbits[4], maskbits[5],
+                                                    maskbits[6], maskbits[7]}},
+                                        co, nnz, kB.p, order, d_vals, out.vals.p);
+  } else {
+    gather_kernel<<<grid, 256, 0, st>>>(co, nnz, order, d_vals, out.vals.p);
+  }
   SB_CHECK_LAUNCH(ctx);
+  kB.release();
   pA.release();
   pB.release();
 
