@@ -123,7 +123,9 @@ const char*   splatt_version(void);
  * splatt_comm_unique_id: rank 0 only; writes 128 bytes (ncclUniqueId), to be
  * broadcast by the caller (e.g. torch.distributed).  splatt_ctx_set_comm: collective
  * over the nranks ranks (ncclCommInitRank).  NCCL is loaded at run time
- * (libnccl.so.2); failure -> SPLATT_ERR_NCCL.                                      */
+ * (libnccl.so.2); failure -> SPLATT_ERR_NCCL.  id128 = NULL (nranks 1) removes the
+ * communicator; nranks = 1 with an id creates a one-rank NCCL communicator, which runs
+ * the sharded code path (partition, compaction, collectives) on a single GPU.         */
 splatt_status splatt_comm_unique_id(void* id128);
 splatt_status splatt_ctx_set_comm(splatt_ctx* ctx, const void* id128, int nranks, int rank);
 

@@ -168,8 +168,16 @@ class Context:
     def sync(self):
         _raise(lib().splatt_ctx_sync(self._p), self._p)
 
-    def set_comm(self, group=None):
-        """Create the NCCL communicator of this rank from a torch.distributed group."""
+    def set_comm(self, group=None, single=False):
+        """Create the NCCL communicator of this rank from a torch.distributed group, or
+        (single=True, no process group needed) a one-rank NCCL communicator that runs the
+        sharded path on this GPU alone."""
+        if single:
+            buf = (C.c_char * 128)()
+            _raise(lib().splatt_comm_unique_id(buf))
+            _raise(lib().splatt_ctx_set_comm(self._p, buf, 1, 0), self._p)
+            self.nranks, self.rank = 1, 0
+            return
         import torch.distributed as dist
         world = dist.get_world_size(group)
         rank = dist.get_rank(group)

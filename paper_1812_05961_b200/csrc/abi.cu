@@ -171,8 +171,11 @@ splatt_status splatt_ctx_set_comm(splatt_ctx* ctx, const void* id128, int nranks
   return guard(ctx, [&] {
     SB_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, "bad nranks/rank");
     SB_CUDA(cudaSetDevice(ctx->device));
-    if (nranks == 1) { ctx->comm.reset(); return; }
-    SB_REQUIRE(id128 != nullptr, "id128 is NULL");
+    if (id128 == nullptr) {  // no communicator: the unsharded single-GPU path
+      SB_REQUIRE(nranks == 1, "id128 is NULL");
+      ctx->comm.reset();
+      return;
+    }
     ctx->comm = make_nccl_comm(id128, nranks, rank);
   });
 }

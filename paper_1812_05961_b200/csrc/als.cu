@@ -99,6 +99,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   const int ld = padded_ld(R);
   const int G = ctx->comm ? ctx->comm->nranks : 1;
   const int me = ctx->comm ? ctx->comm->rank : 0;
+  const bool sharded = ctx->comm != nullptr;  // also a 1-rank communicator (path tests)
   EventTimer tm;
   tm.s = s;
   tm.on = (st != nullptr);
@@ -120,7 +121,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   std::vector<std::unique_ptr<DevCsf>> csf(N);
   for (int n = 0; n < N; ++n) {
     csf[n] = std::make_unique<DevCsf>();
-    if (G == 1) {
+    if (!sharded) {
       bounds[n] = {0, X.dims[n]};
       build_csf(ctx, X.ind, X.vals, X.nnz, N, X.dims, n, *csf[n]);
       continue;
@@ -223,7 +224,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       rows_solve_stats(ctx, M.p, A[n].p, lo, hi, R, ld, L.p, true, n == N - 1, status.p,
                        stats.p);                                           // potrs + stats
       tm.end();
-      if (G > 1) {
+      if (sharded) {
         tm.begin(kComm);
         ctx->comm->allreduce_sum(stats.p, stats_sum_len(R), s);
         ctx->comm->allreduce_max(stats.p + stats_max_off(R), R, s);

@@ -97,3 +97,25 @@ def test_sharded_als_tol_stop(sb):
     for r in range(2):
         assert multi[r]["iters"] == ref["iters"]
         assert abs(multi[r]["fit"] - ref["fit"]) <= ALS_TOL * abs(ref["fit"])
+
+
+def test_nccl_single_rank_sharded_path(sb):
+    """A one-rank NCCL communicator: the real NCCL calls (all-reduce sum/max, grouped
+    broadcasts) and the sharded driver (bincount, C-14 cut, compaction, local CSFs) on
+    this GPU; the model must equal the oracle's."""
+    import torch
+    t = synth.generate((4000, 1100, 7500), 150_000, [("zipf", 1.1)] * 3, "ratings", seed=22)
+    stream = torch.cuda.Stream(0)
+    ctx = sb.Context(0, stream=stream)
+    ctx.set_comm(single=True)
+    with torch.cuda.stream(stream):
+        ind = [torch.from_numpy(a.view(np.int32)).cuda() for a in t.ind]
+        vals = torch.from_numpy(t.vals).cuda()
+    stream.synchronize()
+    res = sb.cpd_als(ind, vals, t.dims, rank=16, max_iters=5, seed=5, ctx=ctx, out_device=False,
+                     stats=True)
+    ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=16, max_iters=5, seed=5)
+    assert res["stats"]["nranks"] == 1 and res["stats"]["t_comm"] > 0
+    for n in range(3):
+        assert rel_fro(res["factors"][n], ref["factors"][n]) <= ALS_TOL
+    assert abs(res["fit"] - ref["fit"]) <= ALS_TOL * abs(ref["fit"])
