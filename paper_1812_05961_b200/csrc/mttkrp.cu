@@ -354,8 +354,14 @@ template <int N>
 void launch_n(splatt_ctx* ctx, DevCsf& c, const double* const* f, double* out, int ld,
               int R, int chunk) {
   const int slots = ld / 4;
-  constexpr int U = (N <= 4) ? SB_MTTKRP_U : 2;
-  constexpr int MB = (N <= 3) ? SB_MTTKRP_MINB : 1;
+#ifndef SB_MTTKRP_U4
+#define SB_MTTKRP_U4 2
+#endif
+#ifndef SB_MTTKRP_MINB4
+#define SB_MTTKRP_MINB4 2
+#endif
+  constexpr int U = (N == 3) ? SB_MTTKRP_U : (N == 4 ? SB_MTTKRP_U4 : 2);
+  constexpr int MB = (N == 3) ? SB_MTTKRP_MINB : (N == 4 ? SB_MTTKRP_MINB4 : 1);
   if (slots <= 2) launch_t<N, 2, U, MB>(ctx, c, f, out, ld, R, chunk);
   else if (slots <= 4) launch_t<N, 4, U, MB>(ctx, c, f, out, ld, R, chunk);
   else if (slots <= 8) launch_t<N, 8, U, MB>(ctx, c, f, out, ld, R, chunk);
