@@ -78,6 +78,7 @@ def lib():
             L.oracle_csf_vals.argtypes = [P, P]
             L.oracle_csf_free.argtypes = [P]
             L.oracle_partition.argtypes = [P, u64, i32, P]
+            L.oracle_csf_alloc.argtypes = [i32, P, i32, P, P, P, P]
             L.oracle_num_threads.restype = i32
             L.oracle_set_threads.argtypes = [i32]
             _lib = L
@@ -268,6 +269,22 @@ def csf_build(dims, ind, vals, root):
     finally:
         L.oracle_csf_free(h)
     return dict(perm=perm, ids=ids, ptr=ptr, vals=vv)
+
+
+# ---------------------------------------------------------------------- C-15
+def csf_alloc(dims, policy):
+    """CSF allocation policy (0 ALL, 1 ONE, 2 TWO).
+    Returns dict(roots=[...], mode_csf=[...N], mode_level=[...N])."""
+    N = len(dims)
+    n = C.c_int(0)
+    roots = np.zeros(N, dtype=np.int32)
+    mc = np.zeros(N, dtype=np.int32)
+    ml = np.zeros(N, dtype=np.int32)
+    st = lib().oracle_csf_alloc(N, _p(_dims(dims)), int(policy), C.byref(n), _p(roots), _p(mc),
+                                _p(ml))
+    if st:
+        raise OracleError(st)
+    return dict(roots=roots[: n.value].tolist(), mode_csf=mc.tolist(), mode_level=ml.tolist())
 
 
 # ---------------------------------------------------------------------- C-14

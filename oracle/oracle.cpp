@@ -21,6 +21,7 @@
  *   C-12 finalise       PAPER.md:203 (line 14 "return lambda, A^(1..3)")
  *   C-13 CSF            PAPER.md:215-218 (compressed sparse fiber tree)
  *   C-14 partition      SURVEY.md §8(e) (optimal contiguous slice split)
+ *   C-15 CSF policy     SPEC.md:128-136 (ONE / TWO / ALL allocations)
  *
  * Numbers: fp64 throughout.  Parallelism (OpenMP) only over
  * independent outputs whose own summation order is fixed, so every result is
@@ -458,6 +459,37 @@ void oracle_csf_vals(void* h, double* v) {
     std::memcpy(v, c->vals.data(), 8 * c->vals.size());
 }
 void oracle_csf_free(void* h) { delete (OracleCsf*)h; }
+
+/* ---------------------------------------------------- C-15 CSF allocation policy */
+/* SPEC.md:128-136 (allocate_csfs), the paper's lock / no-lock dichotomy PAPER.md:469-470:
+ *   ALL (0): one CSF rooted at every mode; every mode is a ROOT traversal (level 0).
+ *   ONE (1): one CSF rooted at the shortest mode (ties -> lowest id), the other modes
+ *            below it by ascending length (C-13's order); mode at level l uses level l.
+ *   TWO (2): ONE's CSF plus a second rooted at the longest mode (the LAST mode of the
+ *            ascending-length order); each root mode uses its own CSF at level 0, every
+ *            other mode uses the first CSF at its level there.
+ * Outputs: *ncsf, roots[ncsf], mode_csf[N] (which CSF), mode_level[N] (its level).  */
+int oracle_csf_alloc(int N, const uint64_t* dims, int policy, int* ncsf, int* roots,
+                     int* mode_csf, int* mode_level) {
+    std::vector<int> asc(N);
+    std::iota(asc.begin(), asc.end(), 0);
+    std::stable_sort(asc.begin(), asc.end(), [&](int a, int b) { return dims[a] < dims[b]; });
+    if (policy == 0) {
+        *ncsf = N;
+        for (int m = 0; m < N; ++m) { roots[m] = m; mode_csf[m] = m; mode_level[m] = 0; }
+        return OR_OK;
+    }
+    if (policy != 1 && policy != 2) return OR_BADINPUT;
+    *ncsf = policy;
+    roots[0] = asc[0];
+    for (int l = 0; l < N; ++l) { mode_csf[asc[l]] = 0; mode_level[asc[l]] = l; }
+    if (policy == 2) {
+        roots[1] = asc[N - 1];
+        mode_csf[asc[N - 1]] = 1;
+        mode_level[asc[N - 1]] = 0;
+    }
+    return OR_OK;
+}
 
 /* ------------------------------------------------------------ C-14 partition */
 /* Cut S slices (weights w) into G contiguous ranges minimising the max weight.

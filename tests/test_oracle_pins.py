@@ -464,3 +464,48 @@ def test_x12_partition_optimal_bruteforce():
             bb = (0,) + cuts + (S,)
             best = min(best, max(int(w[bb[g]:bb[g + 1]].sum()) for g in range(G)))
         assert got == best
+
+
+# ------------------------------------------------------------------ X-13
+def test_x13_spec_csf_alloc_examples():
+    """C-15 against SPEC.md:128-136's allocate_csfs examples (tests/golden/spec_csf_alloc.json)."""
+    g = golden("spec_csf_alloc.json")
+    kind_of = {0: "ROOT"}
+    for case in g["cases"]:
+        a = oracle.csf_alloc(case["dims"], g["policies"][case["policy"]])
+        assert a["roots"] == case["roots"]
+        assert a["mode_csf"] == case["mode_csf"]
+        assert a["mode_level"] == case["mode_level"]
+        N = len(case["dims"])
+        for m in range(N):
+            lvl = a["mode_level"][m]
+            kind = kind_of.get(lvl, "LEAF" if lvl == N - 1 else "INTERNAL")
+            assert kind == case["kinds"][str(m)]
+        for k, perm in enumerate(case.get("perms", [])):
+            assert oracle.csf_perm(case["dims"], a["roots"][k]).tolist() == perm
+
+
+def test_x13_csf_alloc_properties():
+    """Every mode's level is its position in its CSF's level order; ALL is all-root; ONE's
+    root is the shortest mode (ties -> lowest id); TWO adds the longest."""
+    rng = np.random.default_rng(13)
+    for _ in range(200):
+        N = int(rng.integers(3, 9))
+        dims = [int(x) for x in rng.integers(1, 6, N)]
+        for pol in (0, 1, 2):
+            a = oracle.csf_alloc(dims, pol)
+            assert len(a["roots"]) == {0: N, 1: 1, 2: 2}[pol]
+            for m in range(N):
+                perm = oracle.csf_perm(dims, a["roots"][a["mode_csf"][m]]).tolist()
+                assert perm[a["mode_level"][m]] == m
+            if pol == 0:
+                assert a["mode_level"] == [0] * N
+            else:
+                shortest = min(range(N), key=lambda m: (dims[m], m))
+                assert a["roots"][0] == shortest
+                if pol == 2:
+                    longest = max(range(N), key=lambda m: (dims[m], m))
+                    assert a["roots"][1] == longest
+                    assert a["mode_level"][longest] == 0
+    with pytest.raises(oracle.OracleError):
+        oracle.csf_alloc([3, 4, 5], 7)
