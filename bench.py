@@ -16,6 +16,7 @@ NCCL all-reduce / all-gather inside the library ("scaling": "strong", fixed tens
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import os
 import statistics
@@ -46,6 +47,62 @@ def peaks():
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class NvmlClockSampler:
+    """NVML sampling (in-process thread) during the timed region: SM clock, max SM clock
+    and the clock-event (throttle) reasons, the fields of the recipe's clocks line."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, gpu: int, period_s: float = 0.1):
+        self.gpu = gpu
+        self.period = period_s
+        self.sm, self.mx, self.reasons = [], 0.0, set()
+        self.ok = False
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[0].isdigit() else self.gpu
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = pynvml
+            self.ok = True
+        except Exception:
+            return self
+        self.stop = threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                self.mx = max(self.mx, float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self.stop.wait(self.period)
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self.stop.set()
+            self.t.join(timeout=5)
+
+    def summary(self):
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "source": "nvml"}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.mx,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml"}
 
 
 class ClockSampler:
@@ -160,9 +217,10 @@ def run_reference(args, cfg, t):
     print(json.dumps(line), flush=True)
 
 
-def config_block(cfg, G):
+def config_block(cfg, G, policy="all"):
     return {"workload": cfg["name"], "dims": list(cfg["dims"]), "nnz": cfg["nnz"],
             "rank": cfg["rank"], "iters": cfg["iters"], "seed": cfg["seed"],
+            "csf_policy": policy,
             "parallelism": f"slice-partitioned x{G}" if G > 1 else "single GPU",
             "l2": "inputs larger than L2 (COO + per-mode CSFs >> 126 MB); no explicit flush"}
 
@@ -177,6 +235,10 @@ def main():
     ap.add_argument("--iters", type=int, default=None, help="override CP-ALS iterations")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--clocks", default="nvml", choices=["nvml", "smi", "off"],
+                    help="clock sampler during the timed region (nvml: in-process thread)")
+    ap.add_argument("--policy", default="all", choices=["all", "one", "two"],
+                    help="CSF allocation policy (SPLATT_CSF_*)")
     args = ap.parse_args()
 
     import synth
@@ -219,7 +281,7 @@ def main():
 
     def step(stats=True):
         return sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=iters, tol=0.0,
-                          seed=cfg["seed"], ctx=ctx, stats=stats)
+                          seed=cfg["seed"], ctx=ctx, stats=stats, policy=args.policy)
 
     for _ in range(args.warmup):
         step()
@@ -230,7 +292,8 @@ def main():
     runs = []
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    sampler = {"nvml": NvmlClockSampler, "smi": ClockSampler}.get(args.clocks)
+    with (sampler(local) if sampler else contextlib.nullcontext()) as clk:
         torch.cuda.synchronize(local)
         if world > 1:
             dist.barrier()
@@ -262,7 +325,7 @@ def main():
             torch.cuda.synchronize(local)
             a = time.perf_counter()
             r = sb.cpd_als(h_ind, h_val, t.dims, rank=R, max_iters=iters, seed=cfg["seed"],
-                           ctx=ctx, out=h_out)
+                           ctx=ctx, out=h_out, policy=args.policy)
             b = time.perf_counter()
             if k > 0:
                 e_times.append(b - a)
@@ -308,7 +371,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_block(cfg, world),
+        "config": config_block(cfg, world, args.policy),
         "cpals_sec_per_iter": statistics.mean(loop) / iters,
         "mttkrp_nnzR_per_s": N * t.nnz * R * iters * args.steps / t_mttkrp if t_mttkrp else None,
         "breakdown_s_per_step": {k: sum(s[k] for s in st) / args.steps for k in
@@ -321,7 +384,7 @@ def main():
                      "avg_launch_ms": 1e3 * t_mttkrp / max(1, launches),
                      "launches": launches},
         "gpu_launches": sum(s["kernel_launches"] for s in st),
-        "clocks": clk.summary(),
+        "clocks": clk.summary() if clk else None,
         "e2e": e2e,
     }
     if not args.no_cpu_baseline and world == 1:

@@ -54,9 +54,17 @@ typedef enum {
 
 enum { SPLATT_MAX_NMODES = 8, SPLATT_MAX_RANK = 128 };
 
-/* CSF allocation policy.  ALL: one CSF rooted at every mode, so
- * every MTTKRP is a root ("no-lock") traversal.                       */
-enum { SPLATT_CSF_ALL = 0 };
+/* CSF allocation policy (the lock / no-lock dichotomy of
+ * PAPER.md:253-275, 469-470).
+ *   ALL: one CSF rooted at every mode, so every MTTKRP is a ROOT ("no-lock") traversal
+ *        with owned output rows.  N CSFs of memory.
+ *   ONE: one CSF rooted at the shortest mode (ties -> lowest id), the other modes below
+ *        it by ascending length; the mode at level l > 0 runs the INTERNAL (l < N-1) or
+ *        LEAF (l = N-1) kernel, whose output rows are shared between parents and are
+ *        accumulated with fp64 atomics (the GPU's replacement of the paper's mutex pool).
+ *   TWO: ONE's CSF plus one rooted at the longest mode (the last in ascending-length
+ *        order); both roots run ROOT kernels, every other mode its level in the first.  */
+enum { SPLATT_CSF_ALL = 0, SPLATT_CSF_ONE = 1, SPLATT_CSF_TWO = 2 };
 
 typedef struct splatt_ctx splatt_ctx;   /* device, stream, allocator pool, optional comm */
 typedef struct splatt_csf splatt_csf;   /* device-resident CSF set, immutable after build */
@@ -147,8 +155,9 @@ splatt_status splatt_partition(const uint64_t* w, uint64_t S, int32_t G, uint64_
 
 /* ---------------------------------------------------------------- CSF */
 /* Build the CSF set of `coo` on the device (sort = PAPER.md:415).
- * CSF_n (policy ALL) is rooted at mode n; below the root the other modes follow by
- * ascending length, ties to the lower mode id.  Level l < N-1
+ * The policy (SPLATT_CSF_ALL / ONE / TWO above) decides which trees are built: CSF k
+ * is rooted at its root mode (ALL: CSF_n at mode n); below the root the other modes
+ * follow by ascending length, ties to the lower mode id.  Level l < N-1
  * holds ids_l (the level's coordinate) and ptr_l (offsets into level l+1, one
  * extra end entry); the leaf level holds ids_{N-1} and vals in sorted order.
  * Bit-exact: the result is a pure integer function of the input.
@@ -157,6 +166,12 @@ splatt_status splatt_partition(const uint64_t* w, uint64_t S, int32_t G, uint64_
  * policy, mismatch), UNSUPPORTED (nnz >= 2^32).                                     */
 splatt_status splatt_csf_build(splatt_ctx* ctx, const splatt_coo* coo, int32_t nmodes,
                                const uint64_t* dims, int32_t policy, splatt_csf** out);
+/* Allocation of a built CSF set: *ncsf (ALL: N, ONE: 1, TWO: 2) and, for mode `mode`,
+ * the CSF index `which` and the tree level `level` its MTTKRP uses (0 = ROOT, N-1 =
+ * LEAF, else INTERNAL).  Any output may be NULL; `mode` must be in [0, N) unless both
+ * `which` and `level` are NULL.  Host-only, synchronous.                            */
+splatt_status splatt_csf_dispatch(const splatt_csf* csf, int32_t mode, int32_t* ncsf,
+                                  int32_t* which, int32_t* level);
 /* Shape of CSF `which` (0..ncsf-1): mode_perm[0..N) (level -> mode) and n_nodes[l]
  * per level; either may be NULL.  Synchronous, host outputs.                       */
 splatt_status splatt_csf_info(const splatt_csf* csf, int32_t which, int32_t* nmodes,
@@ -174,11 +189,22 @@ void          splatt_csf_free(splatt_csf* csf);
  * for every i < dims[mode], r < rank; rows with no nonzeros are written 0; columns
  * r >= rank of `out` are written 0.  factors: N device pointers (factors[mode] is
  * ignored, may be NULL), each dims[m] x ld.  out: device, dims[mode] x ld.
- * Uses the CSF rooted at `mode`.  Errors: BADINPUT (mode, rank not in [1,128],
+ * Uses the CSF and kernel the build policy assigns to `mode` (splatt_csf_dispatch).
+ * ROOT results are deterministic; INTERNAL/LEAF (policies ONE/TWO) accumulate with
+ * fp64 atomics, so their rounding order varies run to run.  Errors: BADINPUT (mode,
+ * rank not in [1,128],
  * ld < rank, NULL pointers).  Asynchronous on the context stream.                  */
 splatt_status splatt_mttkrp(splatt_ctx* ctx, const splatt_csf* csf, int32_t mode,
                             const double* const* factors, int32_t rank, int32_t ld,
                             double* out);
+
+/* As splatt_mttkrp, on CSF `which` of the set (0..ncsf-1) instead of the policy's
+ * choice: the kernel kind follows the level of `mode` in that CSF (ROOT / INTERNAL /
+ * LEAF) — the configuration override of SPEC.md:168, used to test every kernel on every
+ * tree.  Errors: as splatt_mttkrp, plus BADINPUT for `which` out of range.            */
+splatt_status splatt_mttkrp_csf(splatt_ctx* ctx, const splatt_csf* csf, int32_t which,
+                                int32_t mode, const double* const* factors, int32_t rank,
+                                int32_t ld, double* out);
 
 /* ---------------------------------------------------------------- CP-ALS */
 /* Algorithm 1 for an N-mode tensor, fixed readings DESIGN.md §2:
@@ -195,7 +221,10 @@ splatt_status splatt_cpd_als(splatt_ctx* ctx, const splatt_coo* coo, int32_t ran
                              splatt_kruskal* out);
 /* As splatt_cpd_als, plus: init_factors (NULL = seeded init; else N pointers,
  * host or device, I_n x rank, ld = rank, used as the initial A_n), policy
- * (SPLATT_CSF_ALL), stats (NULL or filled; see splatt_stats).                      */
+ * (SPLATT_CSF_ALL / ONE / TWO: which CSFs are built and which MTTKRP kernel each mode
+ * runs; the result differs only by rounding), stats (NULL or filled; see splatt_stats).
+ * A sharded context (splatt_ctx_set_comm*) requires SPLATT_CSF_ALL (UNSUPPORTED
+ * otherwise: row ownership per rank needs a ROOT traversal for every mode).          */
 splatt_status splatt_cpd_als_ex(splatt_ctx* ctx, const splatt_coo* coo, int32_t rank,
                                 int32_t max_iters, double tol, uint64_t seed,
                                 const double* const* init_factors, int32_t policy,

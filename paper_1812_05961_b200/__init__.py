@@ -20,13 +20,17 @@ import threading
 import numpy as np
 
 __all__ = ["lib", "Context", "Loopback", "Csf", "csf_build", "mttkrp", "cpd_als", "partition",
-           "SplattError", "SingularError", "EmptyTensorError", "STATUS", "padded_ld"]
+           "SplattError", "SingularError", "EmptyTensorError", "STATUS", "padded_ld",
+           "CSF_ALL", "CSF_ONE", "CSF_TWO", "POLICIES"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SPLATT_B200_LIB") or os.path.join(_HERE, "libsplatt_b200.so")
 MAX_NMODES = 8
 MAX_RANK = 128
 CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
+
+CSF_ALL, CSF_ONE, CSF_TWO = 0, 1, 2  # SPLATT_CSF_* (include/splatt_b200.h)
+POLICIES = {"all": CSF_ALL, "one": CSF_ONE, "two": CSF_TWO}
 
 STATUS = {0: "OK", -1: "BADINPUT", -2: "NOMEM", -3: "SINGULAR", -4: "CUDA", -5: "NCCL",
           -6: "EMPTY", -7: "UNSUPPORTED"}
@@ -108,6 +112,9 @@ def lib():
                 "splatt_csf_export": (st, [P, i32, i32, P, P, P]),
                 "splatt_csf_free": (None, [P]),
                 "splatt_mttkrp": (st, [P, P, i32, P, i32, i32, P]),
+                "splatt_mttkrp_csf": (st, [P, P, i32, i32, P, i32, i32, P]),
+                "splatt_csf_dispatch": (st, [P, i32, C.POINTER(i32), C.POINTER(i32),
+                                             C.POINTER(i32)]),
                 "splatt_cpd_als": (st, [P, C.POINTER(Coo), i32, i32, f64, u64, C.POINTER(Kruskal)]),
                 "splatt_cpd_als_ex": (st, [P, C.POINTER(Coo), i32, i32, f64, u64, P, i32,
                                            C.POINTER(Kruskal), C.POINTER(Stats)]),
@@ -284,6 +291,19 @@ class Csf:
         self.ctx = ctx
         self.dims = tuple(int(d) for d in dims)
 
+    @property
+    def ncsf(self) -> int:
+        n = C.c_int32()
+        _raise(lib().splatt_csf_dispatch(self._p, 0, C.byref(n), None, None), self.ctx.ptr)
+        return n.value
+
+    def dispatch(self, mode: int):
+        """(which CSF, level) the policy assigns to `mode` (level 0 ROOT, N-1 LEAF)."""
+        w, l = C.c_int32(), C.c_int32()
+        _raise(lib().splatt_csf_dispatch(self._p, mode, None, C.byref(w), C.byref(l)),
+               self.ctx.ptr)
+        return w.value, l.value
+
     def info(self, which: int):
         n = C.c_int32()
         perm = np.zeros(MAX_NMODES, dtype=np.int32)
@@ -321,8 +341,14 @@ class Csf:
             pass
 
 
-def csf_build(ind, vals, dims, ctx: Context | None = None, policy: int = 0) -> Csf:
-    """splatt_csf_build: one CSF per mode (policy ALL).  ind/vals host or device."""
+def _policy(policy) -> int:
+    return POLICIES[policy.lower()] if isinstance(policy, str) else int(policy)
+
+
+def csf_build(ind, vals, dims, ctx: Context | None = None, policy=CSF_ALL) -> Csf:
+    """splatt_csf_build under `policy` (CSF_ALL / CSF_ONE / CSF_TWO or "all"/"one"/"two").
+    ind/vals host or device."""
+    policy = _policy(policy)
     ctx = ctx or default_context()
     ind = [_as_u32(a) for a in ind]
     vals = _as_f64(vals)
@@ -333,9 +359,11 @@ def csf_build(ind, vals, dims, ctx: Context | None = None, policy: int = 0) -> C
     return Csf(p, ctx, dims)
 
 
-def mttkrp(csf: Csf, mode: int, factors, out=None, rank: int | None = None):
-    """splatt_mttkrp.  factors: list of N float64 CUDA tensors (I_m x ld, row-major);
-    factors[mode] may be None.  Returns out (I_mode x ld)."""
+def mttkrp(csf: Csf, mode: int, factors, out=None, rank: int | None = None,
+           which: int | None = None):
+    """splatt_mttkrp (or splatt_mttkrp_csf on CSF `which`).  factors: list of N float64
+    CUDA tensors (I_m x ld, row-major); factors[mode] may be None.  Returns out
+    (I_mode x ld)."""
     import torch
     ctx = csf.ctx
     ref = next(f for m, f in enumerate(factors) if m != mode and f is not None)
@@ -345,14 +373,18 @@ def mttkrp(csf: Csf, mode: int, factors, out=None, rank: int | None = None):
         out = torch.empty((csf.dims[mode], ld), dtype=torch.float64, device=ref.device)
     arr = (C.c_void_p * len(factors))(*[(_ptr(f) if f is not None and m != mode else None)
                                         for m, f in enumerate(factors)])
-    _raise(lib().splatt_mttkrp(ctx.ptr, csf._p, mode, arr, R, int(out.stride(0)), _ptr(out)),
-           ctx.ptr)
+    if which is None:
+        code = lib().splatt_mttkrp(ctx.ptr, csf._p, mode, arr, R, int(out.stride(0)), _ptr(out))
+    else:
+        code = lib().splatt_mttkrp_csf(ctx.ptr, csf._p, int(which), mode, arr, R,
+                                       int(out.stride(0)), _ptr(out))
+    _raise(code, ctx.ptr)
     return out
 
 
 def cpd_als(ind, vals, dims, rank: int, max_iters: int, tol: float = 0.0, seed: int = 0,
             init=None, ctx: Context | None = None, out_device: bool = True, stats: bool = False,
-            out=None):
+            out=None, policy=CSF_ALL):
     """splatt_cpd_als(_ex).  Returns dict(factors, lam, fit, iters, fit_history[, stats]).
 
     ind/vals may be host (numpy / CPU tensors) or CUDA tensors; outputs are CUDA
@@ -389,7 +421,8 @@ def cpd_als(ind, vals, dims, rank: int, max_iters: int, tol: float = 0.0, seed: 
         init_arr = (C.c_void_p * N)(*[_ptr(a) for a in init])
     st = Stats() if stats else None
     code = lib().splatt_cpd_als_ex(ctx.ptr, C.byref(coo), rank, max_iters, float(tol), int(seed),
-                                   init_arr, 0, C.byref(kr), C.byref(st) if st else None)
+                                   init_arr, _policy(policy), C.byref(kr),
+                                   C.byref(st) if st else None)
     _raise(code, ctx.ptr)
     res = dict(factors=fac, lam=lam, fit=kr.fit, iters=kr.iters,
                fit_history=hist[: kr.iters].copy())

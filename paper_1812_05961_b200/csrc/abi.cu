@@ -194,7 +194,8 @@ splatt_status splatt_csf_build(splatt_ctx* ctx, const splatt_coo* coo, int32_t n
     SB_REQUIRE(nmodes == coo->nmodes, "nmodes disagrees with coo->nmodes");
     SB_REQUIRE(dims != nullptr, "dims is NULL");
     for (int m = 0; m < nmodes; ++m) SB_REQUIRE(dims[m] == coo->dims[m], "dims disagree with coo");
-    SB_REQUIRE(policy == SPLATT_CSF_ALL, "unknown CSF policy");
+    SB_REQUIRE(policy == SPLATT_CSF_ALL || policy == SPLATT_CSF_ONE || policy == SPLATT_CSF_TWO,
+               "unknown CSF policy");
     SB_CUDA(cudaSetDevice(ctx->device));
     StagedCoo X(ctx, coo);
     if (!validate_coo_device(ctx, X.view.ind, X.view.nnz, nmodes, X.view.dims))
@@ -203,12 +204,12 @@ splatt_status splatt_csf_build(splatt_ctx* ctx, const splatt_coo* coo, int32_t n
     c->N = nmodes;
     c->policy = policy;
     c->ctx = ctx;
-    c->ncsf = nmodes;
     for (int m = 0; m < nmodes; ++m) c->dims[m] = coo->dims[m];
-    for (int n = 0; n < nmodes; ++n) {
-      c->csf[n] = std::make_unique<DevCsf>();
-      build_csf(ctx, X.view.ind, X.view.vals, X.view.nnz, nmodes, X.view.dims, n, *c->csf[n]);
-      c->mode_csf[n] = n;
+    int roots[SPLATT_MAX_NMODES];
+    csf_policy(nmodes, c->dims, policy, &c->ncsf, roots, c->mode_csf, c->mode_level);
+    for (int k = 0; k < c->ncsf; ++k) {
+      c->csf[k] = std::make_unique<DevCsf>();
+      build_csf(ctx, X.view.ind, X.view.vals, X.view.nnz, nmodes, X.view.dims, roots[k], *c->csf[k]);
     }
     *out = c.release();
   });
@@ -251,46 +252,78 @@ void splatt_csf_free(splatt_csf* csf) {
   delete csf;
 }
 
+splatt_status splatt_csf_dispatch(const splatt_csf* csf, int32_t mode, int32_t* ncsf,
+                                  int32_t* which, int32_t* level) {
+  if (!csf) return SPLATT_ERR_BADINPUT;
+  if ((which || level) && (mode < 0 || mode >= csf->N)) return SPLATT_ERR_BADINPUT;
+  if (ncsf) *ncsf = csf->ncsf;
+  if (which) *which = csf->mode_csf[mode];
+  if (level) *level = csf->mode_level[mode];
+  return SPLATT_OK;
+}
+
+namespace {
+
+// MTTKRP of `mode` on CSF `which`: the kernel kind is the level of `mode` in that tree.
+void mttkrp_on(splatt_ctx* ctx, const splatt_csf* csf, int which, int mode,
+               const double* const* factors, int rank, int ld, double* out) {
+  SB_REQUIRE(csf != nullptr && factors != nullptr && out != nullptr, "NULL argument");
+  SB_REQUIRE(mode >= 0 && mode < csf->N, "mode out of range");
+  SB_REQUIRE(which >= 0 && which < csf->ncsf, "CSF index out of range");
+  SB_REQUIRE(rank >= 1 && rank <= SPLATT_MAX_RANK, "rank must be in [1, 128]");
+  SB_REQUIRE(ld >= rank, "ld < rank");
+  const int N = csf->N;
+  for (int m = 0; m < N; ++m)
+    if (m != mode) SB_REQUIRE(factors[m] != nullptr, "factor pointer is NULL");
+  SB_CUDA(cudaSetDevice(ctx->device));
+  DevCsf& c = *csf->csf[which];
+  int level = 0;
+  while (c.perm[level] != mode) ++level;
+  cudaStream_t s = ctx->stream;
+  const int ldi = padded_ld(rank);
+  bool direct = (ld == ldi) && ((uintptr_t)out % 32 == 0);
+  for (int m = 0; m < N; ++m)
+    if (m != mode) direct = direct && ((uintptr_t)factors[m] % 32 == 0);
+  if (direct) {
+    mttkrp_level(ctx, c, level, factors, out, csf->dims[mode], ld, rank);
+    return;
+  }
+  // Staging path: pack factors to the internal padded layout, then copy out.
+  std::vector<DevBuf<double>> F(N);
+  const double* fp[SPLATT_MAX_NMODES] = {nullptr};
+  for (int m = 0; m < N; ++m) {
+    if (m == mode) continue;
+    F[m].alloc(csf->dims[m] * ldi, s);
+    SB_CUDA(cudaMemsetAsync(F[m].p, 0, csf->dims[m] * ldi * 8, s));
+    SB_CUDA(cudaMemcpy2DAsync(F[m].p, ldi * 8, factors[m], (size_t)ld * 8, (size_t)rank * 8,
+                              csf->dims[m], cudaMemcpyDeviceToDevice, s));
+    fp[m] = F[m].p;
+  }
+  DevBuf<double> O(csf->dims[mode] * ldi, s);
+  mttkrp_level(ctx, c, level, fp, O.p, csf->dims[mode], ldi, rank);
+  SB_CUDA(cudaMemsetAsync(out, 0, csf->dims[mode] * (size_t)ld * 8, s));
+  SB_CUDA(cudaMemcpy2DAsync(out, (size_t)ld * 8, O.p, ldi * 8, (size_t)rank * 8, csf->dims[mode],
+                            cudaMemcpyDeviceToDevice, s));
+}
+
+}  // namespace
+
 splatt_status splatt_mttkrp(splatt_ctx* ctx, const splatt_csf* csf, int32_t mode,
                             const double* const* factors, int32_t rank, int32_t ld,
                             double* out) {
   if (!ctx) return SPLATT_ERR_BADINPUT;
   return guard(ctx, [&] {
-    SB_REQUIRE(csf != nullptr && factors != nullptr && out != nullptr, "NULL argument");
+    SB_REQUIRE(csf != nullptr, "NULL argument");
     SB_REQUIRE(mode >= 0 && mode < csf->N, "mode out of range");
-    SB_REQUIRE(rank >= 1 && rank <= SPLATT_MAX_RANK, "rank must be in [1, 128]");
-    SB_REQUIRE(ld >= rank, "ld < rank");
-    const int N = csf->N;
-    for (int m = 0; m < N; ++m)
-      if (m != mode) SB_REQUIRE(factors[m] != nullptr, "factor pointer is NULL");
-    SB_CUDA(cudaSetDevice(ctx->device));
-    DevCsf& c = *csf->csf[csf->mode_csf[mode]];
-    cudaStream_t s = ctx->stream;
-    const int ldi = padded_ld(rank);
-    bool direct = (ld == ldi) && ((uintptr_t)out % 32 == 0);
-    for (int m = 0; m < N; ++m)
-      if (m != mode) direct = direct && ((uintptr_t)factors[m] % 32 == 0);
-    if (direct) {
-      mttkrp_root(ctx, c, factors, out, csf->dims[mode], ld, rank);
-      return;
-    }
-    // Staging path: pack factors to the internal padded layout, then copy out.
-    std::vector<DevBuf<double>> F(N);
-    const double* fp[SPLATT_MAX_NMODES] = {nullptr};
-    for (int m = 0; m < N; ++m) {
-      if (m == mode) continue;
-      F[m].alloc(csf->dims[m] * ldi, s);
-      SB_CUDA(cudaMemsetAsync(F[m].p, 0, csf->dims[m] * ldi * 8, s));
-      SB_CUDA(cudaMemcpy2DAsync(F[m].p, ldi * 8, factors[m], (size_t)ld * 8, (size_t)rank * 8,
-                                csf->dims[m], cudaMemcpyDeviceToDevice, s));
-      fp[m] = F[m].p;
-    }
-    DevBuf<double> O(csf->dims[mode] * ldi, s);
-    mttkrp_root(ctx, c, fp, O.p, csf->dims[mode], ldi, rank);
-    SB_CUDA(cudaMemsetAsync(out, 0, csf->dims[mode] * (size_t)ld * 8, s));
-    SB_CUDA(cudaMemcpy2DAsync(out, (size_t)ld * 8, O.p, ldi * 8, (size_t)rank * 8, csf->dims[mode],
-                              cudaMemcpyDeviceToDevice, s));
+    mttkrp_on(ctx, csf, csf->mode_csf[mode], mode, factors, rank, ld, out);
   });
+}
+
+splatt_status splatt_mttkrp_csf(splatt_ctx* ctx, const splatt_csf* csf, int32_t which,
+                                int32_t mode, const double* const* factors, int32_t rank,
+                                int32_t ld, double* out) {
+  if (!ctx) return SPLATT_ERR_BADINPUT;
+  return guard(ctx, [&] { mttkrp_on(ctx, csf, which, mode, factors, rank, ld, out); });
 }
 
 splatt_status splatt_cpd_als_ex(splatt_ctx* ctx, const splatt_coo* coo, int32_t rank,
@@ -303,7 +336,10 @@ splatt_status splatt_cpd_als_ex(splatt_ctx* ctx, const splatt_coo* coo, int32_t 
     SB_REQUIRE(rank >= 1 && rank <= SPLATT_MAX_RANK, "rank must be in [1, 128]");
     SB_REQUIRE(max_iters >= 1, "max_iters must be >= 1");
     SB_REQUIRE(tol >= 0.0, "tol must be >= 0");
-    SB_REQUIRE(policy == SPLATT_CSF_ALL, "unknown CSF policy");
+    SB_REQUIRE(policy == SPLATT_CSF_ALL || policy == SPLATT_CSF_ONE || policy == SPLATT_CSF_TWO,
+               "unknown CSF policy");
+    if (ctx->comm && policy != SPLATT_CSF_ALL)
+      fail(SPLATT_ERR_UNSUPPORTED, "a sharded context requires policy ALL");
     SB_REQUIRE(out != nullptr && out->lambda != nullptr, "NULL output");
     for (int m = 0; m < coo->nmodes; ++m) SB_REQUIRE(out->factors[m] != nullptr, "NULL factor out");
     if (init_factors)
@@ -317,7 +353,7 @@ splatt_status splatt_cpd_als_ex(splatt_ctx* ctx, const splatt_coo* coo, int32_t 
     o.fit = &out->fit;
     o.iters = &out->iters;
     o.fit_history = out->fit_history;
-    cpd_als_device(ctx, X.view, rank, max_iters, tol, seed, init_factors, o, stats);
+    cpd_als_device(ctx, X.view, rank, max_iters, tol, seed, init_factors, policy, o, stats);
   });
 }
 

@@ -92,7 +92,7 @@ void host_partition(const uint64_t* w, uint64_t S, int G, uint64_t* bounds) {
 }
 
 void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, double tol,
-                    uint64_t seed, const double* const* init, const AlsOut& out,
+                    uint64_t seed, const double* const* init, int policy, const AlsOut& out,
                     splatt_stats* st) {
   cudaStream_t s = ctx->stream;
   const int N = X.N;
@@ -117,15 +117,23 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   if (!(h_normx > 0.0)) fail(SPLATT_ERR_EMPTY, "||X|| = 0");
 
   // ------------------------------------------- partition + CSF build per mode
+  // Unsharded: the policy's CSFs (ALL / ONE / TWO); mode n runs its MTTKRP on
+  // csf[mode_csf[n]] at level mode_level[n].  Sharded: ALL, one local CSF per mode.
+  if (sharded && policy != SPLATT_CSF_ALL)
+    fail(SPLATT_ERR_UNSUPPORTED, "a sharded context requires policy ALL");
+  int ncsf = 0, roots[SPLATT_MAX_NMODES], mode_csf[SPLATT_MAX_NMODES], mode_level[SPLATT_MAX_NMODES];
+  csf_policy(N, X.dims, policy, &ncsf, roots, mode_csf, mode_level);
   std::vector<std::vector<uint64_t>> bounds(N);
-  std::vector<std::unique_ptr<DevCsf>> csf(N);
-  for (int n = 0; n < N; ++n) {
-    csf[n] = std::make_unique<DevCsf>();
-    if (!sharded) {
-      bounds[n] = {0, X.dims[n]};
-      build_csf(ctx, X.ind, X.vals, X.nnz, N, X.dims, n, *csf[n]);
-      continue;
+  std::vector<std::unique_ptr<DevCsf>> csf(std::max(N, ncsf));
+  if (!sharded) {
+    for (int n = 0; n < N; ++n) bounds[n] = {0, X.dims[n]};
+    for (int k = 0; k < ncsf; ++k) {
+      csf[k] = std::make_unique<DevCsf>();
+      build_csf(ctx, X.ind, X.vals, X.nnz, N, X.dims, roots[k], *csf[k]);
     }
+  }
+  for (int n = 0; n < N && sharded; ++n) {
+    csf[n] = std::make_unique<DevCsf>();
     DevBuf<unsigned long long> cnt(X.dims[n], s);
     SB_CUDA(cudaMemsetAsync(cnt.p, 0, X.dims[n] * 8, s));
     histogram_kernel<<<blocks_for(ctx, X.nnz), 256, 0, s>>>(X.ind[n], X.nnz, cnt.p);
@@ -213,9 +221,10 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       tm.begin(kInverse);
       hadamard_cholesky(ctx, Gall.p, N, n, R, L.p, status.p);           // lines 4/7/10 + potrf
       tm.end();
-      if (csf[n]->nnz) {
-        mttkrp_root(ctx, *csf[n], fac, M.p, X.dims[n], ld, R, &tm, kMttkrp);  // lines 5/8/11
-        mttkrp_bytes += mttkrp_alg_bytes(*csf[n], R);
+      DevCsf& cn = *csf[mode_csf[n]];
+      if (cn.nnz) {
+        mttkrp_level(ctx, cn, mode_level[n], fac, M.p, X.dims[n], ld, R, &tm, kMttkrp);  // 5/8/11
+        mttkrp_bytes += mttkrp_alg_bytes(cn, R, mode_level[n]);
         ++mttkrp_launches;
       } else {
         SB_CUDA(cudaMemsetAsync(M.p, 0, X.dims[n] * ld * sizeof(double), s));
@@ -288,8 +297,8 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     st->mttkrp_alg_bytes = mttkrp_bytes;
     st->mttkrp_launches = mttkrp_launches;
     st->kernel_launches = ctx->kernel_launches - launches0;
-    for (int n = 0; n < N; ++n)
-      for (int l = 0; l < N; ++l) st->csf_nodes[n][l] = csf[n]->nodes[l];
+    for (int k = 0; k < (sharded ? N : ncsf); ++k)
+      for (int l = 0; l < N; ++l) st->csf_nodes[k][l] = csf[k]->nodes[l];
     st->iters = it_done;
     st->nranks = G;
   }

@@ -22,9 +22,10 @@ struct AlsOut {
 };
 
 // Algorithm 1 on a device COO (validated here).  init: NULL or N pointers (host or
-// device, ld = R).  Throws sb::Error.
+// device, ld = R).  policy: SPLATT_CSF_ALL / ONE / TWO (ALL only when sharded).
+// Throws sb::Error.
 void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, double tol,
-                    uint64_t seed, const double* const* init, const AlsOut& out,
+                    uint64_t seed, const double* const* init, int policy, const AlsOut& out,
                     splatt_stats* st);
 
 // C-14 partition (host).

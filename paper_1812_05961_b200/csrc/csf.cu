@@ -179,8 +179,29 @@ void csf_perm(int N, const uint64_t* dims, int root, int* perm) {
   for (int m = 0; m < N; ++m)
     if (m != root) rest.push_back(m);
   std::stable_sort(rest.begin(), rest.end(), [&](int a, int b) { return dims[a] < dims[b]; });
-  perm[0] = root;
-  for (int k = 0; k < N - 1; ++k) perm[k + 1] = rest[k];
+  int k = 0;
+  if (root >= 0) perm[k++] = root;  // root < 0: every mode by ascending length
+  for (int m : rest) perm[k++] = m;
+}
+
+void csf_policy(int N, const uint64_t* dims, int policy, int* ncsf, int* roots, int* mode_csf,
+                int* mode_level) {
+  if (policy == SPLATT_CSF_ALL) {
+    *ncsf = N;
+    for (int n = 0; n < N; ++n) { roots[n] = n; mode_csf[n] = n; mode_level[n] = 0; }
+    return;
+  }
+  SB_REQUIRE(policy == SPLATT_CSF_ONE || policy == SPLATT_CSF_TWO, "unknown CSF policy");
+  int order[SPLATT_MAX_NMODES];
+  csf_perm(N, dims, -1, order);  // all modes by ascending length (no root)
+  *ncsf = (policy == SPLATT_CSF_ONE) ? 1 : 2;
+  roots[0] = order[0];
+  for (int l = 0; l < N; ++l) { mode_csf[order[l]] = 0; mode_level[order[l]] = l; }
+  if (policy == SPLATT_CSF_TWO) {
+    roots[1] = order[N - 1];
+    mode_csf[order[N - 1]] = 1;
+    mode_level[order[N - 1]] = 0;
+  }
 }
 
 bool validate_coo_device(splatt_ctx* ctx, const uint32_t* const* d_ind, uint64_t nnz, int N,

@@ -29,6 +29,16 @@ struct DevCsf {
 // (SPEC.md:131).
 void csf_perm(int N, const uint64_t* dims, int root, int* perm);
 
+// CSF allocation policy (PAPER.md:469-470 lock vs no-lock): number of
+// CSFs, their roots, and for every mode the CSF and level its MTTKRP runs on.
+//   ALL: CSF_n rooted at n, every mode at level 0 (ROOT kernel).
+//   ONE: one CSF rooted at the shortest mode (ties -> lower id), the rest by ascending
+//        length below it; mode at level l -> level-l kernel (INTERNAL / LEAF).
+//   TWO: ONE's CSF plus one rooted at the longest mode (last in ascending-length order);
+//        both roots -> ROOT on their CSF, the rest -> their level in the first CSF.
+void csf_policy(int N, const uint64_t* dims, int policy, int* ncsf, int* roots, int* mode_csf,
+                int* mode_level);
+
 // Build CSF rooted at `root` from a device COO (ind[m], vals; nnz entries).
 void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_vals, uint64_t nnz,
                int N, const uint64_t* dims, int root, DevCsf& out);
@@ -48,6 +58,7 @@ struct splatt_csf {
   int policy = SPLATT_CSF_ALL;
   int ncsf = 0;
   std::unique_ptr<sb::DevCsf> csf[SPLATT_MAX_NMODES];
-  int mode_csf[SPLATT_MAX_NMODES] = {0};
+  int mode_csf[SPLATT_MAX_NMODES] = {0};    // CSF used for mode n's MTTKRP
+  int mode_level[SPLATT_MAX_NMODES] = {0};  // level of mode n in that CSF
   splatt_ctx* ctx = nullptr;
 };

@@ -1,0 +1,453 @@
+// mttkrp_kernel.cuh — the CSF MTTKRP kernel template for sm_100a, any output level D
+// (Alg. 1 lines 5/8/11).
+// Included by mttkrp.cu (N = 3), mttkrp_n4.cu (N = 4) and mttkrp_nx.cu (N = 5..8), which
+// instantiate it; nothing else includes it.
+//
+// For CSF levels l = 0..N-1 (mode perm[l] at level l) and output level D:
+//
+//   M[i, :] = sum over level-D nodes with id i of
+//               ( prod_{l < D} A_l[ancestor_l, :] )  (*)  S_D(node)            (elementwise)
+//   S_l(node) = sum_{children c} A_{l+1}[c] (*) S_{l+1}(c)   for l < N-2 ... (bottom-up),
+//   S_{N-2}(fiber) = sum_{leaves k} v_k A_{N-1}[k, :]
+//
+// D = 0 is the root ("no-lock") traversal: rows are owned, written with plain stores.
+// D = 1..N-2 is the INTERNAL kernel, D = N-1 the LEAF kernel:
+// the same output row is reached from many parents, so rows are accumulated with fp64
+// atomics (RED.E.ADD.F64) into the zero-filled output — the GPU's answer to the paper's
+// mutex pool.
+//
+// Design:
+//  * Work unit = a fixed chunk of CH consecutive leaves of the CSF, handled by a lane
+//    group of G lanes (G = next pow2 of ld/4; each lane owns 4 consecutive columns
+//    and moves them with one 256-bit load).  Fixed-size leaf chunks balance the
+//    power-law slices (a 13.8M-nonzero slice is just many chunks) — SURVEY.md §8(a')1a.
+//  * A group walks its chunk in batches of 32 leaves.  Per batch, lane-parallel: load
+//    windows of leaf ids/values (streamed, L1 no-allocate) and of every internal
+//    level's ptr, turn them into 32-bit "node closes here" masks (segment flags derived
+//    from ptr, §8(a')2), and resolve for every leaf how many levels it closes and, per
+//    closed level l, either the id of the closed node (l >= D: bottom-up factor rows and
+//    the output row) or the id of the NEXT node (l < D: the top-down prefix product of
+//    the ancestors' rows must be rebuilt for the following leaf).  One record per leaf
+//    goes to a per-group shared-memory table.
+//  * Then the group runs the batch's leaves in order with register accumulators per
+//    level: a leaf row is FMA'd into the fiber accumulator; a closing node multiplies
+//    its accumulator by its own factor row and pushes it one level up; a closing level-D
+//    node emits (prefix (*) accumulator) to its output row.  The rows of U leaves (and of
+//    the nodes they close/open) are issued before any is consumed (§8(a')4).
+//  * D = 0: slices wholly inside a chunk are written with plain 256-bit stores; the <= 2
+//    slices per chunk that cross a chunk seam go through a per-chunk seam row and fp64
+//    atomics at the chunk end (no atomics in the leaf loop).
+#pragma once
+#include <algorithm>
+
+#include "csf.hpp"
+
+namespace sb {
+namespace mk {
+
+template <int N>
+struct Args {
+  const uint32_t* ids[N];
+  const uint32_t* ptr[N];     // levels 0..N-2
+  const double* fac[N];       // fac[l] = factor of mode perm[l]; fac[D] unused
+  uint32_t nodes[N];
+  const double* vals;
+  double* out;
+  const uint32_t* tab;
+  double* seam;               // D = 0: nchunks x ld, the chunk's first slice if it began earlier
+  uint32_t nnz, nchunks, chunk;
+  uint32_t ld;
+  int R;
+};
+
+struct d4 { double x, y, z, w; };
+
+__device__ __forceinline__ d4 ldg_row(const double* p) {
+  d4 r;
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_stream_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_row(double* p, const d4& v) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z),
+               "d"(v.w) : "memory");
+}
+__device__ __forceinline__ void atomic_row(double* p, const d4& v) {
+  atomicAdd(p + 0, v.x);
+  atomicAdd(p + 1, v.y);
+  atomicAdd(p + 2, v.z);
+  atomicAdd(p + 3, v.w);
+}
+// Columns >= R of the output are written 0 whatever the factors' pad columns hold
+// (every column is computed independently, so pads never touch real columns).
+__device__ __forceinline__ d4 mask_pad(d4 v, int col, int R) {
+  if (col + 0 >= R) v.x = 0.0;
+  if (col + 1 >= R) v.y = 0.0;
+  if (col + 2 >= R) v.z = 0.0;
+  if (col + 3 >= R) v.w = 0.0;
+  return v;
+}
+__device__ __forceinline__ uint32_t lowmask(uint32_t n) {
+  return n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
+}
+template <int G>
+__device__ __forceinline__ uint32_t group_or(uint32_t m, unsigned gmask) {
+#pragma unroll
+  for (int o = G / 2; o >= 1; o >>= 1) m |= __shfl_xor_sync(gmask, m, o, G);
+  return m;
+}
+__device__ __forceinline__ void fma4(d4& acc, double v, const d4& r) {
+  acc.x = fma(v, r.x, acc.x);
+  acc.y = fma(v, r.y, acc.y);
+  acc.z = fma(v, r.z, acc.z);
+  acc.w = fma(v, r.w, acc.w);
+}
+__device__ __forceinline__ void fma4v(d4& acc, const d4& a, const d4& r) {
+  acc.x = fma(a.x, r.x, acc.x);
+  acc.y = fma(a.y, r.y, acc.y);
+  acc.z = fma(a.z, r.z, acc.z);
+  acc.w = fma(a.w, r.w, acc.w);
+}
+__device__ __forceinline__ d4 mul4(const d4& a, const d4& b) {
+  return d4{a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w};
+}
+__device__ __forceinline__ d4 scale4(double v, const d4& a) {
+  return d4{v * a.x, v * a.y, v * a.z, v * a.w};
+}
+
+// Per-leaf record written by the lane-parallel phase.  Word 0: leaf row id; word 1:
+// closing depth d (levels d..N-2 close at this leaf; N-1 = none) | 0x100 if (D = 0) the
+// closing slice is the chunk's first slice and began in an earlier chunk (its row goes
+// to the chunk's seam row and is added to the output with atomics at the chunk end);
+// word 2 + l (l = 0..N-2, only for closed levels l >= d): l >= D: the closed node's id
+// (for D = 0, l = 0: the output row, or the chunk id for a seam slice); l < D: the id of
+// the next node at level l (0 past the end).
+template <int N>
+struct MetaLayout {
+  static constexpr int kWords = ((2 + (N - 1)) + 3) / 4 * 4;
+  static constexpr int kVec = kWords / 4;
+};
+
+constexpr int kBatch = 32;
+constexpr int kBlock = 256;
+
+template <int N>
+__host__ __device__ constexpr int group_smem_words() {
+  return MetaLayout<N>::kWords * kBatch + 2 * kBatch;  // meta + values (doubles)
+}
+
+template <int N, int D, int G, int U, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> a) {
+  constexpr int E = kBatch / G;             // window entries per lane
+  constexpr int NB = (D < N - 1) ? (N - 2 - D) : 0;  // bottom-up factor levels D+1..N-2
+  constexpr int NBA = NB > 0 ? NB : 1;
+  constexpr int NP = D;                      // top-down prefix levels 0..D-1
+  constexpr int NPA = NP > 0 ? NP : 1;
+  constexpr int MV = MetaLayout<N>::kVec;
+  constexpr int KW = MetaLayout<N>::kWords;
+  extern __shared__ __align__(16) uint32_t smem[];
+  const int lane = threadIdx.x & 31;
+  const int q = lane & (G - 1);
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  const uint32_t gib = threadIdx.x / G;  // group in block
+  uint32_t* gs = smem + gib * group_smem_words<N>();
+  uint4* meta = reinterpret_cast<uint4*>(gs);
+  double* sval = reinterpret_cast<double*>(gs + KW * kBatch);
+  const uint32_t group = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const uint32_t ngroups = gridDim.x * blockDim.x / G;
+  const bool active = 4u * q < a.ld;
+  const uint32_t col = 4u * q;
+  // Idle lanes (4q >= ld) re-read column 0..3 so every load is unconditional and valid.
+  const uint32_t colc = active ? col : 0u;
+  const double* __restrict__ fleaf = a.fac[N - 1] + colc;
+
+  for (uint32_t c = group; c < a.nchunks; c += ngroups) {
+    const uint32_t k0 = c * a.chunk;
+    const uint32_t k1 = min(k0 + a.chunk, a.nnz);
+    uint32_t base[N - 1];
+#pragma unroll
+    for (int l = 0; l < N - 1; ++l) base[l] = a.tab[(size_t)c * N + l];
+    const bool first_partial = (D == 0) && (a.tab[(size_t)c * N + N - 1] & 1u);
+    const uint32_t slice0 = base[0];
+    d4 acc[N - 1];
+#pragma unroll
+    for (int l = 0; l < N - 1; ++l) acc[l] = d4{0, 0, 0, 0};
+    // Q[l] = prod_{k <= l} A_k[ancestor_k] for the node containing the current leaf.
+    d4 Q[NPA];
+    if constexpr (NP > 0) {
+#pragma unroll
+      for (int l = 0; l < NP; ++l) {
+        const d4 r = ldg_row(a.fac[l] + colc + (size_t)a.ids[l][base[l]] * a.ld);
+        Q[l] = (l == 0) ? r : mul4(Q[l > 0 ? l - 1 : 0], r);
+      }
+    }
+    int last_dep = N - 1;
+
+    for (uint32_t kb = k0; kb < k1; kb += kBatch) {
+      const uint32_t nb = min((uint32_t)kBatch, k1 - kb);
+      // ---- lane-parallel phase: masks, then one record per leaf into shared memory
+      uint32_t msk[N - 1];
+      {
+        uint32_t m = 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint32_t idx = base[N - 2] + 1 + q + e * G;
+          if (idx <= a.nodes[N - 2]) {
+            const uint32_t pos = a.ptr[N - 2][idx] - 1u - kb;
+            if (pos < nb) m |= 1u << pos;
+          }
+        }
+        msk[N - 2] = group_or<G>(m, gmask);
+      }
+#pragma unroll
+      for (int l = N - 3; l >= 0; --l) {
+        uint32_t m = 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint32_t idx = base[l] + 1 + q + e * G;
+          if (idx <= a.nodes[l]) {
+            const uint32_t pos = a.ptr[l][idx] - 1u - base[l + 1];
+            if (pos < 32u) m |= 1u << pos;
+          }
+        }
+        msk[l] = group_or<G>(m, gmask);
+      }
+      uint32_t cnt[N - 1];
+      cnt[N - 2] = __popc(msk[N - 2]);
+#pragma unroll
+      for (int l = N - 3; l >= 0; --l) cnt[l] = __popc(msk[l] & lowmask(cnt[l + 1]));
+
+      // Record word of a closed level-l node (index `node`).
+      auto level_word = [&](int l, uint32_t node) -> uint32_t {
+        if (l >= D) return a.ids[l][node];
+        return (node + 1u < a.nodes[l]) ? a.ids[l][node + 1u] : 0u;
+      };
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint32_t t = q + e * G;
+        uint32_t w[KW];
+#pragma unroll
+        for (int z = 0; z < KW; ++z) w[z] = 0u;
+        double v = 0.0;
+        uint32_t dep = N - 1;
+        if (t < nb) {
+          w[0] = ld_stream_u32(a.ids[N - 1] + kb + t);
+          v = ld_stream_f64(a.vals + kb + t);
+          if ((msk[N - 2] >> t) & 1u) {
+            uint32_t li = __popc(msk[N - 2] & lowmask(t));
+            uint32_t node = base[N - 2] + li;
+            dep = N - 2;
+            w[2 + (N - 2)] = level_word(N - 2, node);
+#pragma unroll
+            for (int l = N - 3; l >= 0; --l) {
+              if (dep == (uint32_t)(l + 1) && ((msk[l] >> li) & 1u)) {
+                li = __popc(msk[l] & lowmask(li));
+                node = base[l] + li;
+                dep = l;
+                if (D == 0 && l == 0) {
+                  if (first_partial && node == slice0) { dep |= 0x100u; w[2] = c; }
+                  else w[2] = a.ids[0][node];
+                } else {
+                  w[2 + l] = level_word(l, node);
+                }
+              }
+            }
+          }
+        }
+        w[1] = dep;
+#pragma unroll
+        for (int z = 0; z < MV; ++z)
+          meta[t * MV + z] = make_uint4(w[4 * z], w[4 * z + 1], w[4 * z + 2], w[4 * z + 3]);
+        sval[t] = v;
+      }
+      __syncwarp(gmask);
+
+      // ---- sequential phase: U leaves at a time, all row loads issued first
+      for (uint32_t t0 = 0; t0 < nb; t0 += U) {
+        d4 row[U];
+        d4 mid[U][NBA];
+        d4 nxt[U][NPA];
+        uint32_t dep[U], orow[U];
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t t = t0 + u;
+          uint32_t w[KW];
+#pragma unroll
+          for (int z = 0; z < MV; ++z) {
+            const uint4 m4 = meta[t * MV + z];
+            w[4 * z] = m4.x; w[4 * z + 1] = m4.y; w[4 * z + 2] = m4.z; w[4 * z + 3] = m4.w;
+          }
+          v[u] = sval[t];
+          dep[u] = w[1];
+          orow[u] = (D == N - 1) ? w[0] : w[2 + (D < N - 1 ? D : 0)];
+          if constexpr (D < N - 1) row[u] = ldg_row(fleaf + (size_t)w[0] * a.ld);
+          const uint32_t d = w[1] & 0xffu;
+#pragma unroll
+          for (int l = D + 1; l <= N - 2; ++l)
+            if (d <= (uint32_t)l)
+              mid[u][l - D - 1] = ldg_row(a.fac[l] + colc + (size_t)w[2 + l] * a.ld);
+#pragma unroll
+          for (int l = 0; l < NP; ++l)
+            if (d <= (uint32_t)l) nxt[u][l] = ldg_row(a.fac[l] + colc + (size_t)w[2 + l] * a.ld);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (t0 + u < nb) {
+            const uint32_t d = dep[u] & 0xffu;
+            if constexpr (D < N - 1) {
+              fma4(acc[N - 2], v[u], row[u]);
+#pragma unroll
+              for (int l = N - 2; l >= D + 1; --l) {
+                if (d <= (uint32_t)l) {
+                  fma4v(acc[l - 1], acc[l], mid[u][l - D - 1]);
+                  acc[l] = d4{0, 0, 0, 0};
+                }
+              }
+              if (d <= (uint32_t)D) {
+                if constexpr (D == 0) {
+                  double* dst = (dep[u] & 0x100u) ? a.seam : a.out;
+                  if (active) st_row(dst + (size_t)orow[u] * a.ld + col, mask_pad(acc[0], col, a.R));
+                } else {
+                  if (active)
+                    atomic_row(a.out + (size_t)orow[u] * a.ld + col,
+                               mask_pad(mul4(acc[D], Q[NP > 0 ? NP - 1 : 0]), col, a.R));
+                }
+                acc[D] = d4{0, 0, 0, 0};
+              }
+            } else {  // LEAF kernel: every leaf scatters v * prefix into its own row
+              if (active)
+                atomic_row(a.out + (size_t)orow[u] * a.ld + col,
+                           mask_pad(scale4(v[u], Q[NP > 0 ? NP - 1 : 0]), col, a.R));
+            }
+            if constexpr (NP > 0) {
+              // Levels d..D-1 open new nodes at the next leaf: rebuild their prefixes.
+#pragma unroll
+              for (int l = 0; l < NP; ++l)
+                if (d <= (uint32_t)l) Q[l] = (l == 0) ? nxt[u][0] : mul4(Q[l > 0 ? l - 1 : 0], nxt[u][l]);
+            }
+          }
+        }
+      }
+      last_dep = (int)(meta[(nb - 1) * MV].y & 0xffu);
+      __syncwarp(gmask);
+#pragma unroll
+      for (int l = 0; l < N - 1; ++l) base[l] += cnt[l];
+    }
+    if constexpr (D == 0) {
+      // Chunk seams: the first slice (if it began earlier) and the still-open levels
+      // (< last_dep) of the last slice go out through fp64 atomics.
+      if (first_partial && base[0] != slice0 && active) {  // the first slice closed here
+        const double* sp = a.seam + (size_t)c * a.ld + col;  // written by this same lane
+        const d4 r = d4{sp[0], sp[1], sp[2], sp[3]};
+        atomic_row(a.out + (size_t)a.ids[0][slice0] * a.ld + col, r);
+      }
+      if (last_dep > 0) {
+#pragma unroll
+        for (int l = N - 2; l >= 1; --l) {
+          if (l < last_dep) {
+            const uint32_t nid = a.ids[l][base[l]];
+            const d4 r = ldg_row(a.fac[l] + colc + (size_t)nid * a.ld);
+            fma4v(acc[l - 1], acc[l], r);
+          }
+        }
+        if (active) {
+          const uint32_t i = a.ids[0][base[0]];
+          atomic_row(a.out + (size_t)i * a.ld + col, mask_pad(acc[0], col, a.R));
+        }
+      }
+    } else if constexpr (D < N - 1) {
+      // The level-D node still open at the chunk end (and its open descendants).
+      if (last_dep > D) {
+#pragma unroll
+        for (int l = N - 2; l >= D + 1; --l) {
+          if (l < last_dep) {
+            const uint32_t nid = a.ids[l][base[l]];
+            const d4 r = ldg_row(a.fac[l] + colc + (size_t)nid * a.ld);
+            fma4v(acc[l - 1], acc[l], r);
+          }
+        }
+        if (active) {
+          const uint32_t i = a.ids[D][base[D]];
+          atomic_row(a.out + (size_t)i * a.ld + col,
+                     mask_pad(mul4(acc[D], Q[NP > 0 ? NP - 1 : 0]), col, a.R));
+        }
+      }
+    }
+  }
+}
+
+template <int N, int D, int G, int U, int MINB>
+void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, double* out,
+              int ld, int R, int chunk) {
+  Args<N> a{};
+  for (int l = 0; l < N; ++l) {
+    a.ids[l] = c.ids[l].p;
+    a.ptr[l] = (l < N - 1) ? c.ptr[l].p : nullptr;
+    a.fac[l] = (l == D) ? nullptr : fac_by_mode[c.perm[l]];
+    a.nodes[l] = (uint32_t)c.nodes[l];
+  }
+  a.vals = c.vals.p;
+  a.out = out;
+  a.tab = c.tab.p;
+  if (D == 0) {
+    if (c.seam.n < c.nchunks * (size_t)ld) c.seam.alloc(c.nchunks * (size_t)ld, ctx->stream);
+    a.seam = c.seam.p;
+  }
+  a.nnz = (uint32_t)c.nnz;
+  a.nchunks = (uint32_t)c.nchunks;
+  a.chunk = (uint32_t)chunk;
+  a.ld = (uint32_t)ld;
+  a.R = R;
+  // 256 threads per block unless the per-group tables would exceed 160 KB (many small
+  // groups with many levels); the kernel indexes groups by blockDim, not kBlock.
+  int threads = kBlock;
+  while (threads > 64 && (size_t)(threads / G) * group_smem_words<N>() * 4 > 160 * 1024)
+    threads /= 2;
+  const int groups_per_block = threads / G;
+  const size_t smem = (size_t)groups_per_block * group_smem_words<N>() * 4;
+  static bool attr = false;
+  if (!attr) {
+    SB_CUDA(cudaFuncSetAttribute(mttkrp_csf_kernel<N, D, G, U, MINB>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    attr = true;
+  }
+  const uint64_t blocks = ceil_div(c.nchunks, groups_per_block);
+  mttkrp_csf_kernel<N, D, G, U, MINB>
+      <<<(unsigned)std::max<uint64_t>(1, blocks), threads, smem, ctx->stream>>>(a);
+  SB_CHECK_LAUNCH(ctx);
+}
+
+// Lane-group width by ld (G = next pow2 of ld/4); GSET restricts the instantiated widths
+// for the rarely used N >= 5 (a wider group only idles more lanes).
+template <int N, int D, int U, int MB, bool ALLG>
+void launch_g(splatt_ctx* ctx, DevCsf& c, const double* const* f, double* out, int ld, int R,
+              int chunk) {
+  const int slots = ld / 4;
+  if constexpr (ALLG) {
+    if (slots <= 2) return launch_t<N, D, 2, U, MB>(ctx, c, f, out, ld, R, chunk);
+    if (slots <= 4) return launch_t<N, D, 4, U, MB>(ctx, c, f, out, ld, R, chunk);
+    if (slots <= 16 && slots > 8) return launch_t<N, D, 16, U, MB>(ctx, c, f, out, ld, R, chunk);
+  }
+  if (slots <= 8) return launch_t<N, D, 8, U, MB>(ctx, c, f, out, ld, R, chunk);
+  return launch_t<N, D, 32, U, MB>(ctx, c, f, out, ld, R, chunk);
+}
+
+}  // namespace mk
+
+// Per-N entry points (mttkrp.cu / mttkrp_n4.cu / mttkrp_nx.cu): launch the level-D kernel.
+void mttkrp_launch_n3(splatt_ctx*, DevCsf&, int D, const double* const*, double*, int, int, int);
+void mttkrp_launch_n4(splatt_ctx*, DevCsf&, int D, const double* const*, double*, int, int, int);
+void mttkrp_launch_nx(splatt_ctx*, DevCsf&, int D, const double* const*, double*, int, int, int);
+
+}  // namespace sb

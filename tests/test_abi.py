@@ -73,6 +73,15 @@ def test_bad_args_return_status_without_device(L):
     assert L.splatt_mttkrp(None, None, 0, None, 1, 1, None) == -1
     assert L.splatt_cpd_als(None, None, 1, 1, 0.0, 0, None) == -1
     assert L.splatt_partition(None, 0, 0, None) == -1
+    assert L.splatt_mttkrp_csf(None, None, 0, 0, None, 1, 1, None) == -1
+    assert L.splatt_csf_dispatch(None, 0, None, None, None) == -1
+
+
+def test_policy_constants_match_header():
+    import paper_1812_05961_b200 as sb
+    txt = open(HEADER).read()
+    for name, val in (("ALL", sb.CSF_ALL), ("ONE", sb.CSF_ONE), ("TWO", sb.CSF_TWO)):
+        assert re.search(rf"SPLATT_CSF_{name}\s*=\s*{val}\b", txt), name
 
 
 def test_no_cpu_fallback_in_binding():
