@@ -70,6 +70,8 @@ class NvmlClockSampler:
             idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[0].isdigit() else self.gpu
             self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
             self.nv = pynvml
+            # the max-clock query costs ~3 ms of driver time: once, outside the sampling loop
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
             self.ok = True
         except Exception:
             return self
@@ -83,7 +85,6 @@ class NvmlClockSampler:
         while not self.stop.is_set():
             try:
                 self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
-                self.mx = max(self.mx, float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)))
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for k, bit in self.REASONS.items():
                     if r & bit:
@@ -112,8 +113,9 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu: int):
+    def __init__(self, gpu: int, period_s: float = 0.2):
         self.gpu = gpu
+        self.period_ms = max(100, int(period_s * 1000))
         self.proc = None
         self.lines = []
 
@@ -121,7 +123,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -228,7 +230,7 @@ def config_block(cfg, G, policy="all"):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -237,6 +239,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--clocks", default="nvml", choices=["nvml", "smi", "off"],
                     help="clock sampler during the timed region (nvml: in-process thread)")
+    ap.add_argument("--clock-period", type=float, default=0.1,
+                    help="seconds between clock samples")
     ap.add_argument("--policy", default="all", choices=["all", "one", "two"],
                     help="CSF allocation policy (SPLATT_CSF_*)")
     args = ap.parse_args()
@@ -279,9 +283,22 @@ def main():
         vals = torch.from_numpy(t.vals).cuda(local)
     torch.cuda.synchronize(local)
 
+    host_call_s = []
+    # Caller-owned device outputs, allocated once (a repeated-solve caller's pattern): the
+    # timed region holds the library call, not torch allocator traffic.
+    dev_out = {"factors": [torch.empty((int(d), R), dtype=torch.float64, device=f"cuda:{local}")
+                           for d in t.dims],
+               "lam": torch.empty(R, dtype=torch.float64, device=f"cuda:{local}")}
+
     def step(stats=True):
-        return sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=iters, tol=0.0,
-                          seed=cfg["seed"], ctx=ctx, stats=stats, policy=args.policy)
+        t0 = time.perf_counter()
+        try:
+            r = sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=iters, tol=0.0,
+                           seed=cfg["seed"], ctx=ctx, stats=stats, policy=args.policy,
+                           out=dev_out)
+            return {"stats": r["stats"], "fit": r["fit"]}
+        finally:
+            host_call_s.append(time.perf_counter() - t0)
 
     for _ in range(args.warmup):
         step()
@@ -293,7 +310,7 @@ def main():
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     sampler = {"nvml": NvmlClockSampler, "smi": ClockSampler}.get(args.clocks)
-    with (sampler(local) if sampler else contextlib.nullcontext()) as clk:
+    with (sampler(local, args.clock_period) if sampler else contextlib.nullcontext()) as clk:
         torch.cuda.synchronize(local)
         if world > 1:
             dist.barrier()
@@ -376,7 +393,10 @@ def main():
         "mttkrp_nnzR_per_s": N * t.nnz * R * iters * args.steps / t_mttkrp if t_mttkrp else None,
         "breakdown_s_per_step": {k: sum(s[k] for s in st) / args.steps for k in
                                  ("t_build", "t_mttkrp", "t_inverse", "t_ata", "t_norm", "t_fit",
-                                  "t_comm", "t_loop")},
+                                  "t_comm", "t_loop", "t_call", "t_host_sync", "t_aux_inverse",
+                                  "t_aux_fit")},
+        "host_syncs_per_step": sum(s["host_syncs"] for s in st) / args.steps,
+        "host_call_ms": 1e3 * statistics.mean(host_call_s[-args.steps:]),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "mttkrp_root_kernel", "peak_source": peak_src,

@@ -92,7 +92,9 @@ typedef struct {
 
 /* Per-call measurements, filled by splatt_cpd_als_ex when non-NULL.  Times are
  * seconds from CUDA events on the context stream, summed over the call, in the
- * categories of Table III plus COMM; counters are exact.            */
+ * categories of Table III plus COMM; counters are exact.  The R x R
+ * inverse and the fit run on a side stream overlapped with the MTTKRP: their spans
+ * (including any wait for a free SM) are reported apart, in t_aux_*.                */
 typedef struct {
   double   t_mttkrp;        /* all MTTKRP launches (incl. output zeroing)               */
   double   t_build;         /* validation + COO->CSF build ("Sort")                     */
@@ -108,6 +110,11 @@ typedef struct {
   uint64_t csf_nodes[SPLATT_MAX_NMODES][SPLATT_MAX_NMODES]; /* [csf][level] local nodes */
   int32_t  iters;
   int32_t  nranks;
+  double   t_call;          /* device time from the call's first to its last stream op   */
+  double   t_host_sync;     /* host seconds spent blocked in the call's stream syncs     */
+  int32_t  host_syncs;      /* host<->device synchronisations inside the call            */
+  double   t_aux_inverse;   /* V^-1 (Hadamard + Gauss-Jordan) spans on the side stream,  */
+  double   t_aux_fit;       /*   and fit spans: overlapped with MTTKRP, not in t_inverse  */
 } splatt_stats;
 
 /* ---------------------------------------------------------------- context */

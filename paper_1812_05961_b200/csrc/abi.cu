@@ -331,6 +331,7 @@ splatt_status splatt_cpd_als_ex(splatt_ctx* ctx, const splatt_coo* coo, int32_t 
                                 const double* const* init_factors, int32_t policy,
                                 splatt_kruskal* out, splatt_stats* stats) {
   if (!ctx) return SPLATT_ERR_BADINPUT;
+  const auto t0 = std::chrono::steady_clock::now();
   return guard(ctx, [&] {
     check_coo(coo);
     SB_REQUIRE(rank >= 1 && rank <= SPLATT_MAX_RANK, "rank must be in [1, 128]");
@@ -353,7 +354,14 @@ splatt_status splatt_cpd_als_ex(splatt_ctx* ctx, const splatt_coo* coo, int32_t 
     o.fit = &out->fit;
     o.iters = &out->iters;
     o.fit_history = out->fit_history;
+    static const bool trace = getenv("SPLATT_TRACE") != nullptr;
+    const auto t1 = std::chrono::steady_clock::now();
     cpd_als_device(ctx, X.view, rank, max_iters, tol, seed, init_factors, policy, o, stats);
+    if (trace)
+      fprintf(stderr, "[splatt trace] cpd_als host: staging %.3f ms, driver %.3f ms\n",
+              std::chrono::duration<double, std::milli>(t1 - t0).count(),
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1)
+                  .count());
   });
 }
 

@@ -9,6 +9,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 
 #include "als.hpp"
@@ -100,20 +101,36 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   const int G = ctx->comm ? ctx->comm->nranks : 1;
   const int me = ctx->comm ? ctx->comm->rank : 0;
   const bool sharded = ctx->comm != nullptr;  // also a 1-rank communicator (path tests)
-  EventTimer tm;
-  tm.s = s;
-  tm.on = (st != nullptr);
+  EventTimer tm, tma;  // main-stream and aux-stream spans
+  tm.init(&ctx->ev_pool, s, st != nullptr);
+  ctx->ensure_aux();
+  cudaStream_t aux = ctx->aux;
+  tma.init(&ctx->ev_pool_aux, aux, st != nullptr);
+  const auto h_start = std::chrono::steady_clock::now();
   uint64_t launches0 = ctx->kernel_launches;
+  const uint64_t syncs0 = ctx->host_syncs;
+  const double sync_s0 = ctx->host_sync_s;
+  cudaEvent_t call_a = nullptr, call_b = nullptr;
+  if (st) {
+    SB_CUDA(cudaEventCreate(&call_a));
+    SB_CUDA(cudaEventCreate(&call_b));
+    SB_CUDA(cudaEventRecord(call_a, s));
+  }
 
   // ---------------------------------------------------------------- validate
   tm.begin(kBuild);
-  if (!validate_coo_device(ctx, X.ind, X.nnz, N, X.dims))
-    fail(SPLATT_ERR_BADINPUT, "index out of range for its mode");
+  PhaseTrace tr(s, "cpd_als");
+  DevBuf<int> bad(1, s);
+  validate_coo_enqueue(ctx, X.ind, X.nnz, N, X.dims, bad.p);
   DevBuf<double> normx(1, s);
   norm_sq(ctx, X.vals, X.nnz, normx.p);
   double h_normx = 0.0;
+  int h_bad = 0;
   SB_CUDA(cudaMemcpyAsync(&h_normx, normx.p, sizeof(double), cudaMemcpyDeviceToHost, s));
-  SB_CUDA(cudaStreamSynchronize(s));
+  SB_CUDA(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  host_sync(ctx);
+  if (h_bad) fail(SPLATT_ERR_BADINPUT, "index out of range for its mode");
+  tr.mark("validate");
   if (!(h_normx > 0.0)) fail(SPLATT_ERR_EMPTY, "||X|| = 0");
 
   // ------------------------------------------- partition + CSF build per mode
@@ -140,7 +157,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     SB_CHECK_LAUNCH(ctx);
     std::vector<uint64_t> hc(X.dims[n]);
     SB_CUDA(cudaMemcpyAsync(hc.data(), cnt.p, X.dims[n] * 8, cudaMemcpyDeviceToHost, s));
-    SB_CUDA(cudaStreamSynchronize(s));
+    host_sync(ctx);
     bounds[n].assign(G + 1, 0);
     host_partition(hc.data(), X.dims[n], G, bounds[n].data());
     const uint32_t lo = (uint32_t)bounds[n][me], hi = (uint32_t)bounds[n][me + 1];
@@ -174,6 +191,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     build_csf(ctx, lp, lval.p, local, N, X.dims, n, *csf[n]);
   }
   tm.end();
+  tr.mark("csf builds");
 
   // -------------------------------------------------------------- factors
   std::vector<DevBuf<double>> A(N);
@@ -193,11 +211,12 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   const double* fac[SPLATT_MAX_NMODES] = {nullptr};
   for (int n = 0; n < N; ++n) fac[n] = A[n].p;
   const size_t RR = (size_t)R * R;
-  DevBuf<double> Gall(N * RR, s), stats(stats_len(R), s), L(RR, s), lambda(R, s), inner(1, s),
+  DevBuf<double> Gall(N * RR, s), stats(stats_len(R), s), Vinv((size_t)ld * ld, s), lambda(R, s), inner(1, s),
       M(maxI * ld, s), fit_hist(max_iters, s), nu(R, s);
   DevBuf<int> status(1, s);
   SB_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int), s));
   SB_CUDA(cudaMemsetAsync(fit_hist.p, 0, max_iters * sizeof(double), s));
+  tm.gap();
   tm.begin(kAta);
   for (int n = 0; n < N; ++n) {   // initial Grams (C-4); factors are replicated
     rows_solve_stats(ctx, nullptr, A[n].p, 0, X.dims[n], R, ld, nullptr, false, false, nullptr,
@@ -215,12 +234,33 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   SB_CUDA(cudaEventCreate(&loop_a));
   SB_CUDA(cudaEventCreate(&loop_b));
   SB_CUDA(cudaEventRecord(loop_a, s));
+  // The R x R steps that do not feed the MTTKRP run on the aux stream, overlapped with
+  // it: V^-1 of mode n is formed as soon as the Grams it needs are final (after mode
+  // n-1's Gram refresh) while the main stream scales A_{n-1} and runs MTTKRP_n; the fit
+  // of an iteration runs there too.  Ordering: ev_ready (main -> aux) after each Gram
+  // refresh, ev_aux (aux -> main) before each solve.  Buffers shared by the two streams
+  // (Vinv, Gall, lambda, inner, status) are written by one side only after the other
+  // side's reads are ordered before it by these two events.
+  const bool fit_on_aux = !(tol > 0.0);  // with tol > 0 the host reads every fit
+  auto launch_aux = [&](int next, bool with_fit, int it) {
+    SB_CUDA(cudaEventRecord(ctx->ev_ready, s));
+    SB_CUDA(cudaStreamWaitEvent(aux, ctx->ev_ready, 0));
+    if (with_fit) {
+      tma.begin(kFit);
+      fit(ctx, Gall.p, N, R, lambda.p, inner.p, normx.p, fit_hist.p + (it - 1), aux);  // line 13
+      tma.end();
+    }
+    if (next >= 0) {
+      tma.begin(kInverse);
+      hadamard_inverse(ctx, Gall.p, N, next, R, ld, Vinv.p, status.p, aux);  // lines 4/7/10
+      tma.end();
+    }
+    SB_CUDA(cudaEventRecord(ctx->ev_aux, aux));
+  };
+  launch_aux(0, false, 0);
   for (int it = 1; it <= max_iters; ++it) {
     for (int n = 0; n < N; ++n) {
       const uint64_t lo = bounds[n][me], hi = bounds[n][me + 1];
-      tm.begin(kInverse);
-      hadamard_cholesky(ctx, Gall.p, N, n, R, L.p, status.p);           // lines 4/7/10 + potrf
-      tm.end();
       DevCsf& cn = *csf[mode_csf[n]];
       if (cn.nnz) {
         mttkrp_level(ctx, cn, mode_level[n], fac, M.p, X.dims[n], ld, R, &tm, kMttkrp);  // 5/8/11
@@ -229,9 +269,11 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       } else {
         SB_CUDA(cudaMemsetAsync(M.p, 0, X.dims[n] * ld * sizeof(double), s));
       }
+      SB_CUDA(cudaStreamWaitEvent(s, ctx->ev_aux, 0));  // V^-1 of mode n is ready
+      tm.gap();
       tm.begin(kInverse);
-      rows_solve_stats(ctx, M.p, A[n].p, lo, hi, R, ld, L.p, true, n == N - 1, status.p,
-                       stats.p);                                           // potrs + stats
+      rows_solve_stats(ctx, M.p, A[n].p, lo, hi, R, ld, Vinv.p, true, n == N - 1, status.p,
+                       stats.p);                                           // M V^-1 + stats
       tm.end();
       if (sharded) {
         tm.begin(kComm);
@@ -242,34 +284,38 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       }
       tm.begin(kNorm);
       lambda_gram(ctx, stats.p, R, it == 1, lambda.p, Gall.p + n * RR, inner.p);  // line 6
+      tm.end();
+      const bool last = (n == N - 1);
+      const bool more = !(last && it == max_iters);
+      launch_aux(more ? (n + 1) % N : -1, last && fit_on_aux, it);
+      tm.gap();
+      tm.begin(kNorm);
       scale_columns(ctx, A[n].p, 0, X.dims[n], R, ld, lambda.p);
       tm.end();
     }
-    tm.begin(kFit);
-    fit(ctx, Gall.p, N, R, lambda.p, inner.p, normx.p, fit_hist.p + (it - 1));   // line 13
-    tm.end();
     it_done = it;
-    if (tol > 0.0 && it >= 2) {
-      double two[2];
-      SB_CUDA(cudaMemcpyAsync(two, fit_hist.p + (it - 2), 2 * sizeof(double),
-                              cudaMemcpyDeviceToHost, s));
-      SB_CUDA(cudaStreamSynchronize(s));
-      if (std::fabs(two[1] - two[0]) < tol) break;                        // C-11
+    if (!fit_on_aux) {
+      SB_CUDA(cudaStreamWaitEvent(s, ctx->ev_aux, 0));
+      tm.gap();
+      tm.begin(kFit);
+      fit(ctx, Gall.p, N, R, lambda.p, inner.p, normx.p, fit_hist.p + (it - 1));   // line 13
+      tm.end();
+      if (it >= 2) {
+        double two[2];
+        SB_CUDA(cudaMemcpyAsync(two, fit_hist.p + (it - 2), 2 * sizeof(double),
+                                cudaMemcpyDeviceToHost, s));
+        host_sync(ctx);
+        if (std::fabs(two[1] - two[0]) < tol) break;                        // C-11
+        tm.gap();
+      }
     }
   }
+  SB_CUDA(cudaStreamWaitEvent(s, ctx->ev_aux, 0));  // the aux stream's last work
   SB_CUDA(cudaEventRecord(loop_b, s));
-  int h_status = 0;
-  SB_CUDA(cudaMemcpyAsync(&h_status, status.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-  SB_CUDA(cudaMemcpyAsync(h_hist.data(), fit_hist.p, max_iters * sizeof(double),
-                          cudaMemcpyDeviceToHost, s));
-  SB_CUDA(cudaStreamSynchronize(s));
-  float loop_ms = 0.f;
-  cudaEventElapsedTime(&loop_ms, loop_a, loop_b);
-  cudaEventDestroy(loop_a);
-  cudaEventDestroy(loop_b);
-  if (h_status) fail(SPLATT_ERR_SINGULAR, "Gram Hadamard product is singular (after ridge)");
 
   // ------------------------------------------------------------- finalise (C-12)
+  // Enqueued before the status is read (one host sync per call end); on SINGULAR the
+  // caller's outputs are unspecified.
   for (int n = 0; n < N; ++n) {
     fold_norms(ctx, Gall.p + n * RR, R, lambda.p, nu.p);
     scale_columns(ctx, A[n].p, 0, X.dims[n], R, ld, nu.p);
@@ -277,15 +323,36 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
                               R * sizeof(double), X.dims[n], cudaMemcpyDefault, s));
   }
   SB_CUDA(cudaMemcpyAsync(out.lambda, lambda.p, R * sizeof(double), cudaMemcpyDefault, s));
-  SB_CUDA(cudaStreamSynchronize(s));
+  int h_status = 0;
+  SB_CUDA(cudaMemcpyAsync(&h_status, status.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SB_CUDA(cudaMemcpyAsync(h_hist.data(), fit_hist.p, max_iters * sizeof(double),
+                          cudaMemcpyDeviceToHost, s));
+  if (st) SB_CUDA(cudaEventRecord(call_b, s));
+  const auto h_enq = std::chrono::steady_clock::now();
+  host_sync(ctx);
+  const auto h_done = std::chrono::steady_clock::now();
+  float loop_ms = 0.f;
+  cudaEventElapsedTime(&loop_ms, loop_a, loop_b);
+  cudaEventDestroy(loop_a);
+  cudaEventDestroy(loop_b);
+  float call_ms = 0.f;
+  if (st) {
+    cudaEventElapsedTime(&call_ms, call_a, call_b);
+    cudaEventDestroy(call_a);
+    cudaEventDestroy(call_b);
+  }
+  if (h_status) fail(SPLATT_ERR_SINGULAR, "Gram Hadamard product is singular (after ridge)");
   *out.fit = h_hist[it_done - 1];
   *out.iters = it_done;
   if (out.fit_history)
     for (int i = 0; i < it_done; ++i) out.fit_history[i] = h_hist[i];
 
   if (st) {
-    double t[kNumCat] = {0};
+    double t[kNumCat] = {0}, ta[kNumCat] = {0};
     tm.collect(t, kNumCat);
+    tma.collect(ta, kNumCat);
+    st->t_aux_inverse = ta[kInverse];
+    st->t_aux_fit = ta[kFit];
     st->t_mttkrp = t[kMttkrp];
     st->t_build = t[kBuild];
     st->t_ata = t[kAta];
@@ -301,7 +368,18 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       for (int l = 0; l < N; ++l) st->csf_nodes[k][l] = csf[k]->nodes[l];
     st->iters = it_done;
     st->nranks = G;
+    st->t_call = call_ms * 1e-3;
+    st->host_syncs = (int32_t)(ctx->host_syncs - syncs0);
+    st->t_host_sync = ctx->host_sync_s - sync_s0;
   }
+  static const bool trace = getenv("SPLATT_TRACE") != nullptr;
+  if (trace)
+    fprintf(stderr, "[splatt trace] driver: enqueue-to-end %.3f ms (host %.3f ms ahead of the "
+            "device at the final sync), epilogue %.3f ms\n",
+            std::chrono::duration<double, std::milli>(h_enq - h_start).count(),
+            std::chrono::duration<double, std::milli>(h_done - h_enq).count(),
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h_done)
+                .count());
 }
 
 }  // namespace sb

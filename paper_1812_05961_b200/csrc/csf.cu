@@ -204,24 +204,30 @@ void csf_policy(int N, const uint64_t* dims, int policy, int* ncsf, int* roots, 
   }
 }
 
-bool validate_coo_device(splatt_ctx* ctx, const uint32_t* const* d_ind, uint64_t nnz, int N,
-                         const uint64_t* dims) {
+void validate_coo_enqueue(splatt_ctx* ctx, const uint32_t* const* d_ind, uint64_t nnz, int N,
+                          const uint64_t* dims, int* d_bad) {
   IndSet s{};
   for (int m = 0; m < N; ++m) { s.p[m] = d_ind[m]; s.dims[m] = dims[m]; }
   s.N = N;
-  DevBuf<int> bad(1, ctx->stream);
-  SB_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
-  validate_kernel<<<grid_for(ctx, nnz), 256, 0, ctx->stream>>>(s, nnz, bad.p);
+  SB_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), ctx->stream));
+  validate_kernel<<<grid_for(ctx, nnz), 256, 0, ctx->stream>>>(s, nnz, d_bad);
   SB_CHECK_LAUNCH(ctx);
+}
+
+bool validate_coo_device(splatt_ctx* ctx, const uint32_t* const* d_ind, uint64_t nnz, int N,
+                         const uint64_t* dims) {
+  DevBuf<int> bad(1, ctx->stream);
+  validate_coo_enqueue(ctx, d_ind, nnz, N, dims, bad.p);
   int h = 0;
   SB_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  SB_CUDA(cudaStreamSynchronize(ctx->stream));
+  host_sync(ctx);
   return h == 0;
 }
 
 void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_vals, uint64_t nnz,
                int N, const uint64_t* dims, int root, DevCsf& out) {
   cudaStream_t st = ctx->stream;
+  PhaseTrace tr(st, "csf_build");
   if (nnz >= (1ull << 31)) fail(SPLATT_ERR_UNSUPPORTED, "nnz >= 2^31 not supported");
   out.N = N;
   out.nnz = nnz;
@@ -250,6 +256,7 @@ void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
   SB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, kA.p, kB.p, pA.p, pB.p, (int)nnz, 0,
                                           64, st));
   temp.alloc(temp_bytes, st);
+  tr.mark("alloc");
   uint32_t* order = nullptr;  // current permutation (sorted position -> input position)
   for (size_t g = 0; g < groups.size(); ++g) {
     KeySpec ks{};
@@ -273,6 +280,7 @@ void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
   }
   kA.release();
   temp.release();
+  tr.mark("pack+sort");
 
   // Sorted coordinates per level and the permuted values.  With one key group the
   // coordinates are decoded from the sorted keys (sequential reads); otherwise they are
@@ -306,6 +314,7 @@ void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
   kB.release();
   pA.release();
   pB.release();
+  tr.mark("decode");
 
   // Node numbering per internal level.
   DevBuf<uint32_t> node[SPLATT_MAX_NMODES];
@@ -321,10 +330,11 @@ void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
   for (int l = 0; l < N - 1; ++l)
     SB_CUDA(cub::DeviceScan::InclusiveSum(temp.p, temp_bytes, node[l].p, node[l].p, (int)nnz, st));
   temp.release();
+  tr.mark("flags+scan");
   std::vector<uint32_t> counts(N, 0);
   for (int l = 0; l < N - 1; ++l)
     SB_CUDA(cudaMemcpyAsync(&counts[l], node[l].p + (nnz - 1), 4, cudaMemcpyDeviceToHost, st));
-  SB_CUDA(cudaStreamSynchronize(st));
+  host_sync(ctx);
   for (int l = 0; l < N - 1; ++l) out.nodes[l] = counts[l];
   out.nodes[N - 1] = nnz;
   for (int l = 0; l < N - 1; ++l) {
@@ -335,6 +345,7 @@ void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
                                                out.ptr[l].p, out.nodes[l], out.nodes[l + 1]);
     SB_CHECK_LAUNCH(ctx);
   }
+  tr.mark("scatter");
   out.ids[N - 1] = std::move(coord[N - 1]);
   out.tab_chunk = 0;
   out.nchunks = 0;

@@ -46,6 +46,10 @@ void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
 // Ensure the chunk table for `chunk` leaves per work unit exists.
 void ensure_chunk_table(splatt_ctx* ctx, DevCsf& c, int chunk);
 
+// Enqueue the validation: *d_bad (device int) becomes nonzero iff some index >= its dim.
+void validate_coo_enqueue(splatt_ctx* ctx, const uint32_t* const* d_ind, uint64_t nnz, int N,
+                          const uint64_t* dims, int* d_bad);
+
 // Device validation: returns true iff every ind[m][p] < dims[m]  (synchronises).
 bool validate_coo_device(splatt_ctx* ctx, const uint32_t* const* d_ind, uint64_t nnz, int N,
                          const uint64_t* dims);

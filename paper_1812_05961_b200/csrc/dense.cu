@@ -75,92 +75,99 @@ __global__ void sum_partials_kernel(const double* __restrict__ part, int P, doub
   if (threadIdx.x == 0) out[0] = s;
 }
 
-// One CTA.  smem: W (R*R) = V; L is built in W's lower triangle while the strict upper
-// triangle keeps V (V is exactly symmetric), and diag keeps V's diagonal for the retry.
-__global__ void hadamard_cholesky_kernel(const double* __restrict__ G_all, int N, int n, int R,
-                                         double* __restrict__ L, int* status) {
+// One CTA: V = *_{m != n} G_m (ascending m) and V^-1 (Alg. 1 line 5's V^dagger,
+// PAPER.md:194; V is SPD, so V^dagger = V^-1) by in-place Gauss-Jordan elimination without
+// pivoting.  On an SPD matrix the k-th Gauss-Jordan pivot is the k-th Schur-complement
+// diagonal d_k = V_kk - sum_{m<k} L_km^2, i.e. the square of the k-th Cholesky pivot, so
+// the failure test of C-7 applies unchanged: fail if d_k <= 1e-12 * max_j V_jj; on failure
+// retry once with V + (1e-12 * trace(V) / R) I; a second failure sets *status.  Output:
+// Vinv, ld x ld (row-major, zero pad rows/columns >= R).  Each step is one parallel pass
+// over the matrix (two barriers), so the kernel is R short steps, not R^2 serial ones.
+__global__ void hadamard_inverse_kernel(const double* __restrict__ G_all, int N, int n, int R,
+                                        int ld, double* __restrict__ Vinv, int* status) {
   extern __shared__ double sm[];
-  double* W = sm;
-  double* diag = sm + R * R;
+  double* A = sm;            // R x R working matrix
+  double* prow = A + R * R;  // pivot row of the current step (R)
+  double* pcol = prow + R;   // pivot column of the current step (R)
   __shared__ int failed;
-  __shared__ double thr, ridge;
+  __shared__ double mxd, ridge;
   const int RR = R * R;
-  for (int e = threadIdx.x; e < RR; e += blockDim.x) {
-    double p = 1.0;
-    bool first = true;
-    for (int m = 0; m < N; ++m) {
-      if (m == n) continue;
-      const double g = G_all[(size_t)m * RR + e];
-      p = first ? g : p * g;
-      first = false;
-    }
-    W[e] = p;
-    if (e / R == e % R) diag[e / R] = p;
-  }
-  __syncthreads();
   for (int attempt = 0; attempt < 2; ++attempt) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < RR; e += blockDim.x) {  // V (re-read for the retry)
+      double p = 1.0;
+      bool first = true;
+      for (int m = 0; m < N; ++m) {
+        if (m == n) continue;
+        const double g = G_all[(size_t)m * RR + e];
+        p = first ? g : p * g;
+        first = false;
+      }
+      A[e] = p;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
       failed = 0;
-      if (attempt == 1) {
-        double tr = 0.0;
-        for (int j = 0; j < R; ++j) tr += diag[j];
+      double mx = 0.0, tr = 0.0;
+      for (int j = 0; j < R; ++j) { mx = fmax(mx, A[j * R + j]); tr += A[j * R + j]; }
+      if (attempt == 0) {
         ridge = 1e-12 * tr / R;
+        mxd = mx;
       } else {
-        ridge = 0.0;
+        for (int j = 0; j < R; ++j) A[j * R + j] += ridge;
+        mxd = mx + ridge;
       }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < RR; e += blockDim.x) {
-      const int i = e / R, j = e % R;
-      if (i == j) W[e] = diag[i] + ridge;
-      else if (i > j) W[e] = W[j * R + i];  // restore the lower triangle from the upper
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double mx = 0.0;
-      for (int j = 0; j < R; ++j) mx = fmax(mx, W[j * R + j]);
-      thr = 1e-12 * mx;
-    }
-    __syncthreads();
-    // Right-looking: after step j, W[i][k] (k > j, i >= k) holds V[i][k] - sum_{m<=j}
-    // L[i][m] L[k][m], accumulated in ascending m — the same sums, in the same order, as
-    // the oracle's Cholesky-Banachiewicz; every step is one parallel pass.
-    for (int j = 0; j < R; ++j) {
-      const double d = W[j * R + j];
-      if (!(d > thr)) { failed = 1; break; }   // uniform: every thread reads the same d
-      const double piv = sqrt(d);
+    const double th = 1e-12 * mxd;  // 1e-12 x max diagonal of the matrix being inverted
+    for (int k = 0; k < R; ++k) {
+      const double d = A[k * R + k];
+      if (!(d > th)) { failed = 1; break; }  // uniform: every thread reads the same d
+      const double inv = 1.0 / d;
+      for (int j = threadIdx.x; j < R; j += blockDim.x) {
+        prow[j] = (j == k) ? inv : A[k * R + j] * inv;
+        pcol[j] = (j == k) ? 0.0 : A[j * R + k];
+      }
       __syncthreads();
-      if (threadIdx.x == 0) W[j * R + j] = piv;
-      for (int i = j + 1 + threadIdx.x; i < R; i += blockDim.x) W[i * R + j] = W[i * R + j] / piv;
-      __syncthreads();
-      // trailing update on a fixed 16 x 16 thread grid (no integer division)
-      const int ti = threadIdx.x >> 4, tk = threadIdx.x & 15;
-      for (int i = j + 1 + ti; i < R; i += 16) {
-        const double lij = W[i * R + j];
-        for (int k = j + 1 + tk; k <= i; k += 16) W[i * R + k] -= lij * W[k * R + j];
+      for (int e = threadIdx.x; e < RR; e += blockDim.x) {
+        const int i = e / R, j = e % R;
+        if (i == k) {
+          A[e] = prow[j];
+        } else if (j == k) {
+          A[e] = -pcol[i] * inv;
+        } else {
+          A[e] = fma(-pcol[i], prow[j], A[e]);
+        }
       }
       __syncthreads();
     }
     __syncthreads();
-    if (!failed) {
-      for (int e = threadIdx.x; e < RR; e += blockDim.x)
-        L[e] = (e % R <= e / R) ? W[e] : 0.0;
-      return;
-    }
-    __syncthreads();
+    if (!failed) break;
   }
-  if (threadIdx.x == 0) *status = 1;
+  if (failed) {
+    if (threadIdx.x == 0) *status = 1;
+    return;
+  }
+  // symmetrise (the elimination rounds the two triangles differently) and pad to ld
+  for (int e = threadIdx.x; e < ld * ld; e += blockDim.x) {
+    const int i = e / ld, j = e % ld;
+    double v = 0.0;
+    if (i < R && j < R) v = 0.5 * (A[i * R + j] + A[j * R + i]);
+    Vinv[e] = v;
+  }
 }
 
 // ------------------------------------------------- row solves + Gram + colmax
-// Per row m (length R): forward L y = m, back L^T x = y (C-7; the pivots are applied
-// as reciprocals, the sums split over two accumulators).  inner = y . y = m . x, the
-// row's share of <X, Z> (C-10).  Persistent CTAs walk tiles of T rows staged in shared
-// memory (stride ld+2 = 2 mod 4 doubles: conflict-free 128-bit accesses): one thread
-// solves one row, the solved tile is written back coalesced, and while it is still in
-// shared memory every thread accumulates a 4x4 block of the partial Gram (rows split
-// into S subsets when there are fewer block pairs than threads) and the column max |a|.
-// Without `solve` the kernel only reads A (initial Grams).
+// Per row m (length R): x = m V^-1 (line 5, with V^-1 from hadamard_cholesky), computed by
+// a lane group of G lanes (lane q owns columns 4q..4q+3, 256-bit shared-memory operands),
+// so every output is an independent length-R dot product (no serial substitution chain).
+// inner += m . x (the row's share of <X, Z>, C-10).  CTAs walk tiles of T = RPG x groups
+// rows staged in shared memory with cp.async (stride ld+2 doubles: conflict-free 128-bit
+// accesses); the solved tile replaces the staged rows, is written back coalesced and,
+// while still in shared memory, every thread accumulates a 4x4 block of the partial Gram
+// (rows split into S subsets when there are fewer block pairs than threads) and a
+// column-max |a| over a row subset.  Without `solve` the kernel only reads A (initial
+// Grams).  Partials are reduced in a fixed order (reduce_stats_kernel): deterministic.
 __device__ __forceinline__ void block_pair(int q, int nb, int& rb, int& cb) {
   int r = 0;
   while (q >= nb - r) { q -= nb - r; ++r; }
@@ -173,31 +180,35 @@ struct RowsArgs {
   double* A;
   uint64_t lo, hi, ntiles;
   int R, ld, T;
-  const double* L;
+  const double* Vinv;
   const int* status;
   double* part;  // gridDim.x x stats_len(R)
   bool solve;
 };
 
-template <int kMaxBP>  // 1 when there are <= 256 block pairs (ld <= 88), else 3
-__global__ void __launch_bounds__(kThreads) solve_gram_kernel(const RowsArgs a) {
+constexpr int kRPG = 4;  // rows per lane group per tile
+
+template <int kMaxBP, int G>  // kMaxBP: 1 when there are <= 256 block pairs (ld <= 88), else 3
+__global__ void __launch_bounds__(kThreads, kMaxBP == 1 ? 2 : 1) solve_gram_kernel(const RowsArgs a) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[kThreads];
   const int R = a.R, ld = a.ld, ldp = ld + 2, T = a.T;
   const size_t SL = (size_t)R * R + R + 1;
   double* out = a.part + (size_t)blockIdx.x * SL;
-  double* Ls = sm;                                   // ld x ld if solve
-  double* rinv = Ls + (a.solve ? ld * ld : 0);       // ld
-  double* tile = rinv + ld;                          // T x ldp
+  double* Ws = sm;                                   // ld x ld if solve (zero pads)
+  double* tile = Ws + (a.solve ? ld * ld : 0);       // T x ldp
   const bool dead = a.status && *a.status;
-  if (a.solve) {
-    for (int e = threadIdx.x; e < ld * ld; e += blockDim.x) {
-      const int j = e / ld, k = e % ld;
-      Ls[e] = (j < R && k < R) ? a.L[j * R + k] : 0.0;
-    }
-    __syncthreads();
-    for (int j = threadIdx.x; j < R; j += blockDim.x) rinv[j] = 1.0 / Ls[j * ld + j];
+  if (a.solve && !dead) {  // Vinv is ld x ld with zero pads: one contiguous async copy
+    const unsigned base = (unsigned)__cvta_generic_to_shared(Ws);
+    for (int e = threadIdx.x; e < ld * ld / 2; e += blockDim.x)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(base + 16 * e),
+                   "l"(a.Vinv + 2 * e));
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
+  const int q = threadIdx.x & (G - 1);
+  const int grp = threadIdx.x / G;
+  const int col = 4 * q;
+  const bool active = col < ld;
   const int nb = ld / 4;
   const int nbp = nb * (nb + 1) / 2;
   const int S = nbp >= kThreads ? 1 : kThreads / nbp;
@@ -206,12 +217,16 @@ __global__ void __launch_bounds__(kThreads) solve_gram_kernel(const RowsArgs a) 
   double g[kMaxBP][16];
 #pragma unroll
   for (int k = 0; k < kMaxBP; ++k) {
-    const int q = (S > 1) ? (int)threadIdx.x % nbp + k * nbp : (int)threadIdx.x + k * kThreads;
+    const int qq = (S > 1) ? (int)threadIdx.x % nbp + k * nbp : (int)threadIdx.x + k * kThreads;
     rb[k] = cb[k] = -1;
-    if ((S > 1 ? (k == 0 && s_id < S) : q < nbp)) block_pair(q, nb, rb[k], cb[k]);
+    if ((S > 1 ? (k == 0 && s_id < S) : qq < nbp)) block_pair(qq, nb, rb[k], cb[k]);
 #pragma unroll
     for (int z = 0; z < 16; ++z) g[k][z] = 0.0;
   }
+  // column max: thread -> column cm (< CW, CW = pow2 >= R) over row subset cs of CS
+  const int CW = R <= 32 ? 32 : (R <= 64 ? 64 : 128);
+  const int CS = kThreads / CW;
+  const int cm = threadIdx.x % CW, cs = threadIdx.x / CW;
   double cmax = 0.0, inner = 0.0;
   const double* src = a.solve ? a.M : a.A;
   for (uint64_t tI = blockIdx.x; tI < a.ntiles && !dead; tI += gridDim.x) {
@@ -221,46 +236,72 @@ __global__ void __launch_bounds__(kThreads) solve_gram_kernel(const RowsArgs a) 
     __syncthreads();
     {  // async 16-byte copies global -> padded tile (no register staging, all in flight)
       const int half = ld / 2;  // 16-byte pairs per row
-      const double* g = src + row0 * ld;
+      const double* gsrc = src + row0 * ld;
       for (int e = threadIdx.x; e < nrows * half; e += blockDim.x) {
         const int r = e / half, c = 2 * (e % half);
         const unsigned dst = (unsigned)__cvta_generic_to_shared(tile + r * ldp + c);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(g + 2 * e));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gsrc + 2 * e));
       }
       asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
     if (a.solve) {
-      for (int t = threadIdx.x; t < nrows; t += blockDim.x) {
-        double* x = tile + t * ldp;
-        for (int j = 0; j < R; ++j) {                 // L y = m
-          const double* Lj = Ls + j * ld;
-          double s0 = x[j], s1 = 0.0;
-          int k = 0;
-#pragma unroll 4
-          for (; k + 1 < j; k += 2) {
-            const double2 xv = *reinterpret_cast<const double2*>(x + k);
-            const double2 lv = *reinterpret_cast<const double2*>(Lj + k);
-            s0 = fma(-lv.x, xv.x, s0);
-            s1 = fma(-lv.y, xv.y, s1);
+      // x[u][0..3] = sum_k m_u[k] Vinv[k][col..col+3] for the group's kRPG rows: each
+      // Vinv operand is loaded once per k for all kRPG rows (register blocking).
+      double x[kRPG][4];
+#pragma unroll
+      for (int u = 0; u < kRPG; ++u) x[u][0] = x[u][1] = x[u][2] = x[u][3] = 0.0;
+      const int r0 = grp * kRPG;
+      if (active && r0 < nrows) {
+        const double* wc = Ws + col;
+        const double* m0 = tile + r0 * ldp;
+        int k = 0;
+        for (; k + 1 < R; k += 2) {
+          const double2 w0a = *reinterpret_cast<const double2*>(wc + k * ld);
+          const double2 w0b = *reinterpret_cast<const double2*>(wc + k * ld + 2);
+          const double2 w1a = *reinterpret_cast<const double2*>(wc + (k + 1) * ld);
+          const double2 w1b = *reinterpret_cast<const double2*>(wc + (k + 1) * ld + 2);
+#pragma unroll
+          for (int u = 0; u < kRPG; ++u) {
+            const double2 mv = *reinterpret_cast<const double2*>(m0 + u * ldp + k);
+            x[u][0] = fma(mv.x, w0a.x, x[u][0]);
+            x[u][1] = fma(mv.x, w0a.y, x[u][1]);
+            x[u][2] = fma(mv.x, w0b.x, x[u][2]);
+            x[u][3] = fma(mv.x, w0b.y, x[u][3]);
+            x[u][0] = fma(mv.y, w1a.x, x[u][0]);
+            x[u][1] = fma(mv.y, w1a.y, x[u][1]);
+            x[u][2] = fma(mv.y, w1b.x, x[u][2]);
+            x[u][3] = fma(mv.y, w1b.y, x[u][3]);
           }
-          if (k < j) s0 = fma(-Lj[k], x[k], s0);
-          const double y = (s0 + s1) * rinv[j];
-          x[j] = y;
-          inner = fma(y, y, inner);
         }
-        for (int j = R - 1; j >= 0; --j) {            // L^T x = y
-          double s0 = x[j], s1 = 0.0;
-          int k = j + 1;
-#pragma unroll 4
-          for (; k + 1 < R; k += 2) {
-            s0 = fma(-Ls[k * ld + j], x[k], s0);
-            s1 = fma(-Ls[(k + 1) * ld + j], x[k + 1], s1);
+        if (k < R) {
+          const double2 wa = *reinterpret_cast<const double2*>(wc + k * ld);
+          const double2 wb = *reinterpret_cast<const double2*>(wc + k * ld + 2);
+#pragma unroll
+          for (int u = 0; u < kRPG; ++u) {
+            const double mk = m0[u * ldp + k];
+            x[u][0] = fma(mk, wa.x, x[u][0]);
+            x[u][1] = fma(mk, wa.y, x[u][1]);
+            x[u][2] = fma(mk, wb.x, x[u][2]);
+            x[u][3] = fma(mk, wb.y, x[u][3]);
           }
-          if (k < R) s0 = fma(-Ls[k * ld + j], x[k], s0);
-          x[j] = (s0 + s1) * rinv[j];
         }
-        for (int j = R; j < ld; ++j) x[j] = 0.0;
+#pragma unroll
+        for (int u = 0; u < kRPG; ++u)
+          if (r0 + u < nrows)
+#pragma unroll
+            for (int z = 0; z < 4; ++z)
+              if (col + z < R) inner = fma(m0[u * ldp + col + z], x[u][z], inner);
+      }
+      __syncthreads();  // every group has read its m rows
+#pragma unroll
+      for (int u = 0; u < kRPG; ++u) {
+        const int r = r0 + u;
+        if (r < nrows && active) {
+          double2* d = reinterpret_cast<double2*>(tile + r * ldp + col);
+          d[0] = make_double2(x[u][0], x[u][1]);
+          d[1] = make_double2(x[u][2], x[u][3]);
+        }
       }
       __syncthreads();
       const int half = ld / 2;
@@ -286,8 +327,8 @@ __global__ void __launch_bounds__(kThreads) solve_gram_kernel(const RowsArgs a) 
           for (int j = 0; j < 4; ++j) g[k][i * 4 + j] = fma(u[i], w[j], g[k][i * 4 + j]);
       }
     }
-    if ((int)threadIdx.x < R)
-      for (int r = 0; r < nrows; ++r) cmax = fmax(cmax, fabs(tile[r * ldp + threadIdx.x]));
+    if (cm < R)
+      for (int r = cs; r < nrows; r += CS) cmax = fmax(cmax, fabs(tile[r * ldp + cm]));
   }
   if (S > 1) {  // combine the row subsets (reuses the tile area)
     double* comb = tile;
@@ -317,7 +358,16 @@ __global__ void __launch_bounds__(kThreads) solve_gram_kernel(const RowsArgs a) 
         }
       }
   }
-  if ((int)threadIdx.x < R) out[(size_t)R * R + 1 + threadIdx.x] = cmax;
+  // column max over the CS row subsets (fixed order), via the shared reduction buffer
+  __syncthreads();
+  red[threadIdx.x] = cmax;
+  __syncthreads();
+  if ((int)threadIdx.x < R) {
+    double mx = 0.0;
+    for (int c = 0; c < CS; ++c) mx = fmax(mx, red[c * CW + threadIdx.x]);
+    out[(size_t)R * R + 1 + threadIdx.x] = mx;
+  }
+  __syncthreads();
   const double tot = block_sum(inner, red);
   if (threadIdx.x == 0) out[(size_t)R * R] = tot;
 }
@@ -436,23 +486,51 @@ void norm_sq(splatt_ctx* ctx, const double* vals, uint64_t nnz, double* d_out) {
   SB_CHECK_LAUNCH(ctx);
 }
 
-void hadamard_cholesky(splatt_ctx* ctx, const double* G_all, int N, int n, int R, double* L,
-                       int* status) {
-  const size_t smem = ((size_t)R * R + R) * sizeof(double);
+void hadamard_inverse(splatt_ctx* ctx, const double* G_all, int N, int n, int R, int ld,
+                      double* Vinv, int* status, cudaStream_t stream) {
+  const size_t smem = ((size_t)R * R + 2 * R) * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
-    SB_CUDA(cudaFuncSetAttribute(hadamard_cholesky_kernel,
+    SB_CUDA(cudaFuncSetAttribute(hadamard_inverse_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (128 * 128 + 128) * 8));
+                                 (128 * 128 + 2 * 128) * 8));
     attr_set = true;
   }
-  hadamard_cholesky_kernel<<<1, kThreads, smem, ctx->stream>>>(G_all, N, n, R, L, status);
+  hadamard_inverse_kernel<<<1, 1024, smem, stream ? stream : ctx->stream>>>(G_all, N, n, R, ld,
+                                                                          Vinv, status);
   SB_CHECK_LAUNCH(ctx);
 }
 
+namespace {
+
+template <int KB, int G>
+void launch_rows(const RowsArgs& a, int P, size_t smem, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    SB_CUDA(cudaFuncSetAttribute(solve_gram_kernel<KB, G>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  solve_gram_kernel<KB, G><<<P, kThreads, smem, s>>>(a);
+}
+
+template <int KB>
+void launch_rows_g(int G, const RowsArgs& a, int P, size_t smem, cudaStream_t s) {
+  switch (G) {
+    case 2: return launch_rows<KB, 2>(a, P, smem, s);
+    case 4: return launch_rows<KB, 4>(a, P, smem, s);
+    case 8: return launch_rows<KB, 8>(a, P, smem, s);
+    case 16: return launch_rows<KB, 16>(a, P, smem, s);
+    default: return launch_rows<KB, 32>(a, P, smem, s);
+  }
+}
+
+}  // namespace
+
 void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, uint64_t hi,
-                      int R, int ld, const double* L, bool solve, bool inner, const int* status,
-                      double* stats) {
+                      int R, int ld, const double* Vinv, bool solve, bool inner,
+                      const int* status, double* stats) {
+  // Vinv: ld x ld, zero pads (hadamard_inverse)
   (void)inner;  // the inner product is always produced by the solve (it is free)
   const size_t SL = stats_len(R);
   cudaStream_t s = ctx->stream;
@@ -461,23 +539,14 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
     return;
   }
   const int ldp = ld + 2;
-  const size_t budget = 190 * 1024;
-  const size_t lbytes = solve ? (size_t)ld * ld * 8 : 0;
+  const int slots = ld / 4;
+  const int G = slots <= 2 ? 2 : slots <= 4 ? 4 : slots <= 8 ? 8 : slots <= 16 ? 16 : 32;
   const int nb = ld / 4, nbp = nb * (nb + 1) / 2;
   const int S = nbp >= kThreads ? 1 : kThreads / nbp;
-  int T = (int)std::min<size_t>(256, (budget - lbytes - (size_t)ld * 8) / ((size_t)ldp * 8));
-  T = std::max(32, T / 32 * 32);
+  const int T = (kThreads / G) * kRPG;
   // the subset-combine buffer aliases the tile
-  while ((size_t)T * ldp < (size_t)S * nbp * 16) T += 32;
-  const size_t smem = lbytes + (size_t)ld * 8 + (size_t)T * ldp * 8;
-  static bool attr_set = false;
-  if (!attr_set) {
-    SB_CUDA(cudaFuncSetAttribute(solve_gram_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 210 * 1024));
-    SB_CUDA(cudaFuncSetAttribute(solve_gram_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 210 * 1024));
-    attr_set = true;
-  }
+  const size_t tile_doubles = std::max<size_t>((size_t)T * ldp, (size_t)S * nbp * 16);
+  const size_t smem = (solve ? (size_t)ld * ld * 8 : 0) + tile_doubles * 8;
   RowsArgs a{};
   a.M = M;
   a.A = A;
@@ -487,15 +556,15 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
   a.ld = ld;
   a.T = T;
   a.ntiles = ceil_div(hi - lo, T);
-  a.L = L;
+  a.Vinv = Vinv;
   a.status = status;
   a.solve = solve;
-  const int per_sm = std::max<int>(1, (int)((228 * 1024) / (smem + 4096)));
-  const int P = (int)std::min<uint64_t>(a.ntiles, (uint64_t)ctx->num_sms * std::min(per_sm, 2));
+  const int per_sm = std::max<int>(1, std::min<int>(2, (int)((228 * 1024) / (smem + 2048))));
+  const int P = (int)std::min<uint64_t>(a.ntiles, (uint64_t)ctx->num_sms * per_sm);
   DevBuf<double> part((size_t)P * SL, s);
   a.part = part.p;
-  if (nbp <= kThreads) solve_gram_kernel<1><<<P, kThreads, smem, s>>>(a);
-  else solve_gram_kernel<3><<<P, kThreads, smem, s>>>(a);
+  if (nbp <= kThreads) launch_rows_g<1>(G, a, P, smem, s);
+  else launch_rows_g<3>(G, a, P, smem, s);
   SB_CHECK_LAUNCH(ctx);
   reduce_stats_kernel<<<(unsigned)ceil_div(SL, kThreads / 32), kThreads, 0, s>>>(part.p, P, R,
                                                                                 stats);
@@ -524,8 +593,9 @@ void scale_columns(splatt_ctx* ctx, double* A, uint64_t lo, uint64_t hi, int R, 
 }
 
 void fit(splatt_ctx* ctx, const double* G_all, int N, int R, const double* lambda,
-         const double* inner, const double* normx_sq, double* fit_out) {
-  fit_kernel<<<1, kThreads, 0, ctx->stream>>>(G_all, N, R, lambda, inner, normx_sq, fit_out);
+         const double* inner, const double* normx_sq, double* fit_out, cudaStream_t stream) {
+  fit_kernel<<<1, kThreads, 0, stream ? stream : ctx->stream>>>(G_all, N, R, lambda, inner,
+                                                                normx_sq, fit_out);
   SB_CHECK_LAUNCH(ctx);
 }
 

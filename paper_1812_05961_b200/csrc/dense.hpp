@@ -19,19 +19,22 @@ void init_factor(splatt_ctx* ctx, double* A, uint64_t I, int R, int ld, uint64_t
 // sum of squares of vals (deterministic two-pass reduction) into d_out[0].
 void norm_sq(splatt_ctx* ctx, const double* vals, uint64_t nnz, double* d_out);
 
-// a5 + a7 (factor): V = *_{m != n} G_m (ascending m), Cholesky V = L L^T with the
-// 1e-12*max diag pivot test and one 1e-12*trace/R ridge retry.  G_all: N x R*R.
-// L: R*R (lower, row-major).  status: set to 1 on failure (never cleared here).
-void hadamard_cholesky(splatt_ctx* ctx, const double* G_all, int N, int n, int R, double* L,
-                       int* status);
+// a5 + a7 (factor): V = *_{m != n} G_m (ascending m) and V^-1 (Alg. 1 line 5's
+// V^dagger) by Gauss-Jordan elimination without pivoting, whose pivots are the Cholesky
+// pivots squared: the C-7 test (pivot <= 1e-12 * max diag) and one 1e-12*trace/R ridge
+// retry apply as stated.  G_all: N x R*R.  Vinv: ld x ld (symmetric, zero pads).
+// status: set to 1 on failure (never cleared here; Vinv then unwritten).
+// Launched on `stream` (default: the context stream).
+void hadamard_inverse(splatt_ctx* ctx, const double* G_all, int N, int n, int R, int ld,
+                      double* Vinv, int* status, cudaStream_t stream = nullptr);
 
 // a7 (solve) + a9/a8/a10 partials: for rows [lo, hi): if solve, A[i,:] = M[i,:] V^-1
-// (forward/back substitution with L); then accumulate the Gram of the rows, the
-// column max |A| and (if inner) sum M .* A.  Reduced to stats (stats_len(R)).
-// If !solve, M is ignored and A is only read.  Skipped when *status != 0.
+// (row times the symmetric inverse from hadamard_inverse, ld x ld); then accumulate the Gram of
+// the rows, the column max |A| and (if inner) sum M .* A.  Reduced to stats
+// (stats_len(R)).  If !solve, M is ignored and A is only read.  Skipped when *status != 0.
 void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, uint64_t hi,
-                      int R, int ld, const double* L, bool solve, bool inner, const int* status,
-                      double* stats);
+                      int R, int ld, const double* Vinv, bool solve, bool inner,
+                      const int* status, double* stats);
 
 // a8 + a9: lambda (first: 2-norm = sqrt(G~_rr); else max(1, colmax)), G_n =
 // G~ / (lambda lambda^T) (mirrored), inner_out = stats inner.
@@ -47,7 +50,8 @@ void scale_columns(splatt_ctx* ctx, double* A, uint64_t lo, uint64_t hi, int R, 
 
 // a10: fit = 1 - sqrt(max(0, nx + zz - 2 inner)) / sqrt(nx), zz = lambda^T (*_m G_m) lambda.
 void fit(splatt_ctx* ctx, const double* G_all, int N, int R, const double* lambda,
-         const double* inner, const double* normx_sq, double* fit_out);
+         const double* inner, const double* normx_sq, double* fit_out,
+         cudaStream_t stream = nullptr);
 
 // a11 (finalise one mode): nu_r = sqrt(G_n[r,r]); lambda_r *= nu_r; nu written to nu.
 void fold_norms(splatt_ctx* ctx, const double* G_n, int R, double* lambda, double* nu);

