@@ -6,10 +6,10 @@
 namespace sb {
 
 #ifndef SB_MTTKRP_U
-#define SB_MTTKRP_U 4
+#define SB_MTTKRP_U 2
 #endif
 #ifndef SB_MTTKRP_MINB
-#define SB_MTTKRP_MINB 2
+#define SB_MTTKRP_MINB 3
 #endif
 
 void mttkrp_launch_n3(splatt_ctx* ctx, DevCsf& c, int D, const double* const* f, double* out,
@@ -23,10 +23,18 @@ void mttkrp_launch_n3(splatt_ctx* ctx, DevCsf& c, int D, const double* const* f,
   }
 }
 
+// Leaves per work unit (measured on B200: c2/c4 best at 256 for N = 3, c5 at 512 for N = 4;
+// shorter chunks balance better, longer ones amortise the per-chunk setup and seam rows).
+#ifndef SB_MTTKRP_CHUNK3
+#define SB_MTTKRP_CHUNK3 256
+#endif
+#ifndef SB_MTTKRP_CHUNK
+#define SB_MTTKRP_CHUNK 512
+#endif
+
 int mttkrp_chunk_leaves(int N, int ld) {
-  (void)N;
   (void)ld;
-  return 512;
+  return N == 3 ? SB_MTTKRP_CHUNK3 : SB_MTTKRP_CHUNK;
 }
 
 double mttkrp_alg_bytes(const DevCsf& c, int R, int level) {
