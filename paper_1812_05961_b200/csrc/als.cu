@@ -190,6 +190,8 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     for (int m = 0; m < N; ++m) lp[m] = lind[m].p;
     build_csf(ctx, lp, lval.p, local, N, X.dims, n, *csf[n]);
   }
+  for (int n = 0; n < N; ++n)  // chunk tables / hot ids before the loop (no syncs inside it)
+    mttkrp_prepare(ctx, *csf[sharded ? n : mode_csf[n]], sharded ? 0 : mode_level[n], ld);
   tm.end();
   tr.mark("csf builds");
 

@@ -234,7 +234,9 @@ void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
   csf_perm(N, dims, root, out.perm);
   int bits[SPLATT_MAX_NMODES];
   const uint32_t* lvl_src[SPLATT_MAX_NMODES];
+  for (int l = 0; l < N; ++l) out.hot_ready[l] = false;
   for (int l = 0; l < N; ++l) {
+    out.dims[l] = dims[out.perm[l]];
     bits[l] = bits_for(dims[out.perm[l]]);
     lvl_src[l] = d_ind[out.perm[l]];
   }

@@ -23,6 +23,11 @@ struct DevCsf {
   uint64_t nchunks = 0;
   DevBuf<uint32_t> tab;
   DevBuf<double> seam;  // MTTKRP scratch: one row per chunk (chunk-seam slices)
+  uint64_t dims[SPLATT_MAX_NMODES] = {0};  // length of the mode at each level
+  // Non-root MTTKRP: the 8 most frequent ids of each level (~0u = unused), computed on
+  // first use of that level as an output level.
+  uint32_t hot[SPLATT_MAX_NMODES][8];
+  bool hot_ready[SPLATT_MAX_NMODES] = {false};
 };
 
 // perm: root first, then the other modes by ascending length, ties to the lower id

@@ -1,5 +1,8 @@
 // mttkrp.cu — CSF MTTKRP host entry points and the N = 3 instantiations (SURVEY.md §8(a)
 // a6, §8(f) NEXT-1).  The kernel is mttkrp_kernel.cuh.
+#include <algorithm>
+#include <vector>
+
 #include "mttkrp.hpp"
 #include "mttkrp_kernel.cuh"
 
@@ -53,6 +56,47 @@ double mttkrp_alg_bytes(const DevCsf& c, int R, int level) {
   return 12.0 * (double)c.nnz + 8.0 * internal + 8.0 * R * rows;
 }
 
+namespace {
+
+__global__ void id_histogram_kernel(const uint32_t* __restrict__ ids, uint64_t n,
+                                    uint32_t* __restrict__ cnt) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
+       j += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[ids[j]], 1u);
+}
+
+// The 8 most frequent ids of CSF level `level` (ties -> lower id), once per tree.
+void ensure_hot(splatt_ctx* ctx, DevCsf& c, int level) {
+  if (c.hot_ready[level]) return;
+  const uint64_t I = c.dims[level], n = c.nodes[level];
+  DevBuf<uint32_t> cnt(I, ctx->stream);
+  SB_CUDA(cudaMemsetAsync(cnt.p, 0, I * 4, ctx->stream));
+  const uint64_t blocks = std::min<uint64_t>(ceil_div(n, 256), (uint64_t)ctx->num_sms * 8);
+  id_histogram_kernel<<<(unsigned)std::max<uint64_t>(1, blocks), 256, 0, ctx->stream>>>(
+      c.ids[level].p, n, cnt.p);
+  SB_CHECK_LAUNCH(ctx);
+  std::vector<uint32_t> h(I);
+  SB_CUDA(cudaMemcpyAsync(h.data(), cnt.p, I * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  host_sync(ctx);
+  std::vector<uint32_t> idx(I);
+  for (uint64_t i = 0; i < I; ++i) idx[i] = (uint32_t)i;
+  const size_t k = std::min<size_t>(8, I);
+  std::partial_sort(idx.begin(), idx.begin() + k, idx.end(), [&](uint32_t a, uint32_t b) {
+    return h[a] != h[b] ? h[a] > h[b] : a < b;
+  });
+  for (int j = 0; j < 8; ++j)
+    c.hot[level][j] = ((size_t)j < k && h[idx[j]] > 1) ? idx[j] : ~0u;
+  c.hot_ready[level] = true;
+}
+
+}  // namespace
+
+void mttkrp_prepare(splatt_ctx* ctx, DevCsf& c, int level, int ld) {
+  if (c.nnz == 0) return;
+  ensure_chunk_table(ctx, c, mttkrp_chunk_leaves(c.N, ld));
+  if (level > 0) ensure_hot(ctx, c, level);
+}
+
 void mttkrp_level(splatt_ctx* ctx, DevCsf& c, int level, const double* const* fac_by_mode,
                   double* out, uint64_t out_rows, int ld, int R, EventTimer* tm, int cat) {
   if (ld % 4 != 0) fail(SPLATT_ERR_BADINPUT, "internal: ld must be a multiple of 4");
@@ -62,6 +106,7 @@ void mttkrp_level(splatt_ctx* ctx, DevCsf& c, int level, const double* const* fa
   if (c.nnz == 0) return;
   const int chunk = mttkrp_chunk_leaves(c.N, ld);
   ensure_chunk_table(ctx, c, chunk);
+  if (level > 0) ensure_hot(ctx, c, level);
   if (tm) tm->begin(cat);
   switch (c.N) {
     case 3: mttkrp_launch_n3(ctx, c, level, fac_by_mode, out, ld, R, chunk); break;

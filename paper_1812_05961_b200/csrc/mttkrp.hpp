@@ -14,6 +14,11 @@ void mttkrp_level(splatt_ctx* ctx, DevCsf& c, int level, const double* const* fa
                   double* out, uint64_t out_rows, int ld, int R, EventTimer* tm = nullptr,
                   int cat = 0);
 
+// Per-tree MTTKRP metadata for output level `level` (chunk table; for level > 0 the hot
+// output ids), built once; mttkrp_level builds it on first use if this was not called.
+// May synchronise the context stream.
+void mttkrp_prepare(splatt_ctx* ctx, DevCsf& c, int level, int ld);
+
 inline void mttkrp_root(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode,
                         double* out, uint64_t out_rows, int ld, int R, EventTimer* tm = nullptr,
                         int cat = 0) {

@@ -58,6 +58,7 @@ struct Args {
   uint32_t nnz, nchunks, chunk;
   uint32_t ld;
   int R;
+  uint32_t hot[8];            // D > 0: the output level's most frequent ids (~0u = none)
 };
 
 struct d4 { double x, y, z, w; };
@@ -150,9 +151,16 @@ __host__ __device__ constexpr int group_smem_words() {
 // (cp.reduce.async.bulk .add.f64, SASS UBLKRED): the group stages the row in shared memory
 // and one lane hands the whole row (ld doubles) to the async-copy engine, instead of ld
 // per-lane fp64 atomics — measured 2.5x the row-update rate on B200.
+// Power-law output ids make a few rows receive most of the updates, and updates to one
+// address serialise at L2: each group keeps private shared-memory accumulators for the
+// kHot most frequent output ids (chosen at CSF build time) and adds them to global memory
+// once, when the group finishes.
 constexpr int kRedBufs = 4;  // staging rows per lane group (ring)
+constexpr int kHot = 8;      // privatised hot output rows per lane group
 template <int D>
-__host__ __device__ constexpr int group_red_doubles(int ld) { return D > 0 ? kRedBufs * ld : 0; }
+__host__ __device__ constexpr int group_red_doubles(int ld) {
+  return D > 0 ? (kRedBufs + kHot) * ld : 0;
+}
 
 template <int N, int D, int G, int U, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> a) {
@@ -182,8 +190,16 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
   double* rbuf = reinterpret_cast<double*>(smem + (blockDim.x / G) * group_smem_words<N>()) +
                  (size_t)gib * group_red_doubles<D>(a.ld);
   uint32_t rslot = 0, rissued = 0;
-  // out[row, :] += v (all lanes of the group call this together).
-  auto emit_row = [&](uint32_t row, const d4& v) {
+  double* hacc = rbuf + kRedBufs * a.ld;  // kHot private rows (D > 0)
+  if constexpr (D > 0) {
+    if (active)
+      for (int h = 0; h < kHot; ++h) {
+        reinterpret_cast<double2*>(hacc + h * a.ld + col)[0] = make_double2(0.0, 0.0);
+        reinterpret_cast<double2*>(hacc + h * a.ld + col)[1] = make_double2(0.0, 0.0);
+      }
+  }
+  // Bulk-reduce one staged row (all lanes of the group call this together).
+  auto bulk_row = [&](uint32_t row, const d4& v) {
     if (q == 0 && rissued >= (uint32_t)kRedBufs)
       asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kRedBufs - 1) : "memory");
     __syncwarp(gmask);
@@ -202,6 +218,22 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
     }
     rslot = (rslot + 1 == (uint32_t)kRedBufs) ? 0 : rslot + 1;
     ++rissued;
+  };
+  // out[row, :] += v: privatised if `row` is a hot id (group-uniform branch), else bulk.
+  auto emit_row = [&](uint32_t row, const d4& v) {
+    int h = -1;
+#pragma unroll
+    for (int k = 0; k < kHot; ++k) h = (row == a.hot[k]) ? k : h;
+    if (h >= 0) {
+      if (active) {
+        double2* p = reinterpret_cast<double2*>(hacc + h * a.ld + col);
+        const double2 p0 = p[0], p1 = p[1];
+        p[0] = make_double2(p0.x + v.x, p0.y + v.y);
+        p[1] = make_double2(p1.x + v.z, p1.y + v.w);
+      }
+    } else {
+      bulk_row(row, v);
+    }
   };
 
   for (uint32_t c = group; c < a.nchunks; c += ngroups) {
@@ -410,7 +442,18 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
       }
     }
   }
-  if constexpr (D > 0) {  // staged rows must be read (and the reductions done) before exit
+  if constexpr (D > 0) {
+    // flush the privatised hot rows, then wait until every staged row has been read (and
+    // reduced) before the shared memory goes away
+    for (int h = 0; h < kHot; ++h) {
+      if (a.hot[h] == ~0u) continue;
+      d4 v{0, 0, 0, 0};
+      if (active) {
+        const double2* p = reinterpret_cast<const double2*>(hacc + h * a.ld + col);
+        v = d4{p[0].x, p[0].y, p[1].x, p[1].y};
+      }
+      bulk_row(a.hot[h], v);
+    }
     if (q == 0 && rissued > 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 }
@@ -452,7 +495,19 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     attr = true;
   }
-  const uint64_t blocks = ceil_div(c.nchunks, groups_per_block);
+  uint64_t blocks = ceil_div(c.nchunks, groups_per_block);
+  if (D > 0) {
+    // persistent grid: each group walks many chunks, so the privatised hot rows are
+    // flushed once per group rather than once per chunk
+    static int occ = 0;
+    if (!occ) {
+      SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &occ, mttkrp_csf_kernel<N, D, G, U, MINB>, threads, smem));
+      occ = std::max(occ, 1);
+    }
+    blocks = std::min<uint64_t>(blocks, (uint64_t)ctx->num_sms * occ);
+    for (int h = 0; h < 8; ++h) a.hot[h] = c.hot[D][h];
+  }
   mttkrp_csf_kernel<N, D, G, U, MINB>
       <<<(unsigned)std::max<uint64_t>(1, blocks), threads, smem, ctx->stream>>>(a);
   SB_CHECK_LAUNCH(ctx);
