@@ -30,6 +30,14 @@ namespace {
 
 thread_local std::string g_noctx_err;
 
+// After a failed call, wait for whatever the call had enqueued: the next call may reuse
+// the context's arena memory (sb::Arena) that this work still touches.
+void quiesce(splatt_ctx* ctx) {
+  if (!ctx) return;
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->aux) cudaStreamSynchronize(ctx->aux);
+}
+
 template <typename F>
 splatt_status guard(splatt_ctx* ctx, F&& f) {
   try {
@@ -38,12 +46,15 @@ splatt_status guard(splatt_ctx* ctx, F&& f) {
     return SPLATT_OK;
   } catch (const Error& e) {
     if (ctx) ctx->err = e.what(); else g_noctx_err = e.what();
+    quiesce(ctx);
     return e.code;
   } catch (const std::bad_alloc&) {
     if (ctx) ctx->err = "host allocation failed";
+    quiesce(ctx);
     return SPLATT_ERR_NOMEM;
   } catch (const std::exception& e) {
     if (ctx) ctx->err = e.what();
+    quiesce(ctx);
     return SPLATT_ERR_CUDA;
   }
 }

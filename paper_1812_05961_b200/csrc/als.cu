@@ -107,6 +107,13 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   cudaStream_t aux = ctx->aux;
   tma.init(&ctx->ev_pool_aux, aux, st != nullptr);
   const auto h_start = std::chrono::steady_clock::now();
+  // Every device buffer of this call comes from the context's arenas (grown to the previous
+  // call's peak, so a repeated call allocates nothing; see sb::Arena).
+  if (!ctx->arena_call) ctx->arena_call = new Arena();
+  if (!ctx->arena_scratch) ctx->arena_scratch = new Arena();
+  ctx->arena_call->reset();
+  ctx->arena_scratch->reset();
+  ArenaScope call_scope(ctx->arena_call, false);
   uint64_t launches0 = ctx->kernel_launches;
   const uint64_t syncs0 = ctx->host_syncs;
   const double sync_s0 = ctx->host_sync_s;

@@ -228,6 +228,11 @@ void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
                int N, const uint64_t* dims, int root, DevCsf& out) {
   cudaStream_t st = ctx->stream;
   PhaseTrace tr(st, "csf_build");
+  // Inside a library call with an arena (cpd_als): temporaries come from the scratch arena,
+  // released when this build returns; the tree itself from the caller's arena.
+  Arena* const out_arena = current_arena();
+  if (out_arena && !ctx->arena_scratch) ctx->arena_scratch = new Arena();
+  ArenaScope scratch(out_arena ? ctx->arena_scratch : nullptr, true);
   if (nnz >= (1ull << 31)) fail(SPLATT_ERR_UNSUPPORTED, "nnz >= 2^31 not supported");
   out.N = N;
   out.nnz = nnz;
@@ -291,11 +296,19 @@ void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
   CoordOut co{};
   co.N = N;
   for (int l = 0; l < N; ++l) {
-    coord[l].alloc(nnz, st);
+    if (l == N - 1) {  // becomes the leaf level of the tree
+      ArenaScope o(out_arena, false);
+      coord[l].alloc(nnz, st);
+    } else {
+      coord[l].alloc(nnz, st);
+    }
     co.src[l] = lvl_src[l];
     co.dst[l] = coord[l].p;
   }
-  out.vals.alloc(nnz, st);
+  {
+    ArenaScope o(out_arena, false);
+    out.vals.alloc(nnz, st);
+  }
   if (groups.size() == 1) {
     KeySpec ks{};
     int sh = 0;
@@ -340,8 +353,11 @@ void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
   for (int l = 0; l < N - 1; ++l) out.nodes[l] = counts[l];
   out.nodes[N - 1] = nnz;
   for (int l = 0; l < N - 1; ++l) {
-    out.ids[l].alloc(out.nodes[l], st);
-    out.ptr[l].alloc(out.nodes[l] + 1, st);
+    {
+      ArenaScope o(out_arena, false);
+      out.ids[l].alloc(out.nodes[l], st);
+      out.ptr[l].alloc(out.nodes[l] + 1, st);
+    }
     const uint32_t* child = (l == N - 2) ? nullptr : node[l + 1].p;
     scatter_level_kernel<<<grid, 256, 0, st>>>(nnz, node[l].p, child, coord[l].p, out.ids[l].p,
                                                out.ptr[l].p, out.nodes[l], out.nodes[l + 1]);

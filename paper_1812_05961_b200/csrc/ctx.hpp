@@ -1,5 +1,6 @@
 // ctx.hpp — the library context: device, stream, stream-ordered allocator, comm.
 #pragma once
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <memory>
@@ -10,6 +11,8 @@
 #include "common.cuh"
 
 namespace sb {
+
+struct Arena;
 
 // Collective interface used by the ALS driver when the path is sharded
 // (SURVEY.md §8(e)).  Implemented over NCCL (comm.cu).
@@ -39,6 +42,8 @@ struct splatt_ctx {
   uint64_t kernel_launches = 0;
   uint64_t host_syncs = 0;       // blocking stream syncs issued by the library
   double host_sync_s = 0.0;      // host seconds spent in them
+  sb::Arena* arena_call = nullptr;       // per-call buffers of cpd_als (see sb::Arena)
+  sb::Arena* arena_scratch = nullptr;    // CSF-build temporaries, reused tree to tree
   std::vector<cudaEvent_t> ev_pool;      // timing events reused across calls (EventTimer)
   std::vector<cudaEvent_t> ev_pool_aux;  // same, for spans on the aux stream
   // Side stream for the R x R work that overlaps the MTTKRP (V^-1 of the next mode, the
@@ -52,7 +57,9 @@ struct splatt_ctx {
     if (ev_ready) cudaEventDestroy(ev_ready);
     if (ev_aux) cudaEventDestroy(ev_aux);
     if (aux) cudaStreamDestroy(aux);
+    delete_arenas();
   }
+  void delete_arenas();
   void ensure_aux() {
     if (aux) return;
     SB_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
@@ -63,32 +70,118 @@ struct splatt_ctx {
 
 namespace sb {
 
-// RAII device buffer on the context's stream-ordered pool (cudaMallocAsync): frees
+// Bump arena for the device memory of one library call.  Offsets are virtual: an
+// allocation that does not fit the current capacity falls back to the stream-ordered pool
+// but still advances the offset, and the peak seen is the capacity the arena grows to at
+// the start of the next call — so repeated calls allocate nothing.  Scopes nest LIFO
+// (ArenaScope restores the offset), which lets a CSF build reuse one scratch region for
+// every tree.  Work on the context stream is stream-ordered, so reusing a region after a
+// scope closes is safe; the call ends with a host sync before the next call resets it.
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, off = 0, peak = 0;
+  ~Arena() { if (base) cudaFree(base); }
+  // At the start of a call (no live allocations): grow to the last call's peak.
+  void reset() {
+    off = 0;
+    if (peak > cap) {
+      if (base) cudaFree(base);
+      base = nullptr;
+      cap = 0;
+      const size_t want = peak + peak / 16;
+      // the overflow of the previous call sits in the stream-ordered pool: hand it back
+      int dev = 0;
+      cudaMemPool_t pool;
+      if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+        cudaMemPoolTrimTo(pool, 0);
+      if (cudaMalloc((void**)&base, want) == cudaSuccess) cap = want;
+      else cudaGetLastError();  // keep working from the pool
+    }
+    peak = 0;
+  }
+  void* take(size_t bytes) {
+    const size_t a = (off + 255) & ~(size_t)255;
+    off = a + bytes;
+    peak = std::max(peak, off);
+    return (off <= cap) ? base + a : nullptr;
+  }
+};
+
+}  // namespace sb
+
+inline void splatt_ctx::delete_arenas() {
+  delete arena_call;
+  delete arena_scratch;
+  arena_call = arena_scratch = nullptr;
+}
+
+namespace sb {
+
+// The arena DevBuf allocations come from on this thread (nullptr: the stream-ordered pool).
+inline Arena*& current_arena() {
+  static thread_local Arena* a = nullptr;
+  return a;
+}
+
+// Make `a` current for the scope; on exit restore the previous arena and release (LIFO)
+// everything `a` handed out inside the scope if `release` is set.
+struct ArenaScope {
+  Arena* a;
+  Arena* prev;
+  size_t mark;
+  bool release;
+  ArenaScope(Arena* arena, bool release_on_exit)
+      : a(arena), prev(current_arena()), mark(arena ? arena->off : 0), release(release_on_exit) {
+    current_arena() = arena;
+  }
+  ~ArenaScope() {
+    if (a && release) a->off = mark;
+    current_arena() = prev;
+  }
+};
+
+// RAII device buffer: from the current arena if one is set (release is then a no-op; the
+// scope reclaims it), else on the context's stream-ordered pool (cudaMallocAsync): frees
 // are stream-ordered, so no host sync is needed between ALS phases.
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
   cudaStream_t s = nullptr;
+  bool pooled = false;  // true: cudaMallocAsync memory owned by this buffer
   DevBuf() = default;
   DevBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
   void alloc(size_t count, cudaStream_t stream) {
     release();
     s = stream;
     n = count;
-    if (count) SB_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), stream));
+    if (!count) return;
+    if (Arena* a = current_arena()) p = static_cast<T*>(a->take(count * sizeof(T)));
+    if (!p) {
+      SB_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), stream));
+      pooled = true;
+    }
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p && pooled) cudaFreeAsync(p, s);
     p = nullptr;
     n = 0;
+    pooled = false;
   }
   ~DevBuf() { release(); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), pooled(o.pooled) {
+    o.p = nullptr;
+    o.n = 0;
+    o.pooled = false;
+  }
   DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s; pooled = o.pooled;
+      o.p = nullptr; o.n = 0; o.pooled = false;
+    }
     return *this;
   }
   T* get() const { return p; }

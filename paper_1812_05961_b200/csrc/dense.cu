@@ -561,6 +561,7 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
   a.solve = solve;
   const int per_sm = std::max<int>(1, std::min<int>(2, (int)((228 * 1024) / (smem + 2048))));
   const int P = (int)std::min<uint64_t>(a.ntiles, (uint64_t)ctx->num_sms * per_sm);
+  ArenaScope scratch(current_arena() ? ctx->arena_scratch : nullptr, true);  // per-launch
   DevBuf<double> part((size_t)P * SL, s);
   a.part = part.p;
   if (nbp <= kThreads) launch_rows_g<1>(G, a, P, smem, s);
