@@ -399,7 +399,8 @@ def main():
         "host_call_ms": 1e3 * statistics.mean(host_call_s[-args.steps:]),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "mttkrp_root_kernel", "peak_source": peak_src,
+                     "kernel": (f"mttkrp_csf_kernel<N={N}> ROOT traversal" if args.policy == "all"
+                                else f"mttkrp_csf_kernel<N={N}> ROOT/INTERNAL/LEAF ({args.policy})"), "peak_source": peak_src,
                      "alg_bytes_per_launch": alg_bytes / max(1, launches),
                      "avg_launch_ms": 1e3 * t_mttkrp / max(1, launches),
                      "launches": launches},
