@@ -103,10 +103,25 @@ __device__ __forceinline__ uint32_t lowmask(uint32_t n) {
 }
 template <int G>
 __device__ __forceinline__ uint32_t group_or(uint32_t m, unsigned gmask) {
+  if constexpr ((G & (G - 1)) == 0) {
 #pragma unroll
-  for (int o = G / 2; o >= 1; o >>= 1) m |= __shfl_xor_sync(gmask, m, o, G);
-  return m;
+    for (int o = G / 2; o >= 1; o >>= 1) m |= __shfl_xor_sync(gmask, m, o, G);
+    return m;
+  } else {
+    return __reduce_or_sync(gmask, m);  // packed groups of G lanes (G not a power of two)
+  }
 }
+
+// Lane groups: G lanes per group (one 4-column slot of the row per lane), 32 / G groups per
+// warp packed side by side.  G need not be a power of two: for R = 33..36 (ld = 36, 9 slots)
+// G = 9 packs 3 groups in a warp (27 active lanes) where a power-of-two width would fit 2
+// groups of 16 with 7 idle lanes each — 1.5x the rows in flight for the same registers.
+template <int G>
+struct Lanes {
+  static constexpr int kPerWarp = 32 / G;
+  static constexpr int kE = (32 + G - 1) / G;  // window entries per lane (32-leaf batches)
+  static __host__ __device__ int groups_per_block(int threads) { return threads / 32 * kPerWarp; }
+};
 __device__ __forceinline__ void fma4(d4& acc, double v, const d4& r) {
   acc.x = fma(v, r.x, acc.x);
   acc.y = fma(v, r.y, acc.y);
@@ -164,7 +179,7 @@ __host__ __device__ constexpr int group_red_doubles(int ld) {
 
 template <int N, int D, int G, int U, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> a) {
-  constexpr int E = kBatch / G;             // window entries per lane
+  constexpr int E = Lanes<G>::kE;           // window entries per lane
   constexpr int NB = (D < N - 1) ? (N - 2 - D) : 0;  // bottom-up factor levels D+1..N-2
   constexpr int NBA = NB > 0 ? NB : 1;
   constexpr int NP = D;                      // top-down prefix levels 0..D-1
@@ -173,21 +188,24 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
   constexpr int KW = MetaLayout<N>::kWords;
   extern __shared__ __align__(16) uint32_t smem[];
   const int lane = threadIdx.x & 31;
-  const int q = lane & (G - 1);
-  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
-  const uint32_t gib = threadIdx.x / G;  // group in block
+  const int gw = lane / G;                    // group in warp
+  if (gw >= Lanes<G>::kPerWarp) return;       // lanes beyond the packed groups: no work
+  const int q = lane - gw * G;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gw * G));
+  const int gpb = Lanes<G>::groups_per_block(blockDim.x);
+  const uint32_t gib = (threadIdx.x >> 5) * Lanes<G>::kPerWarp + gw;  // group in block
   uint32_t* gs = smem + gib * group_smem_words<N>();
   uint4* meta = reinterpret_cast<uint4*>(gs);
   double* sval = reinterpret_cast<double*>(gs + KW * kBatch);
-  const uint32_t group = (blockIdx.x * blockDim.x + threadIdx.x) / G;
-  const uint32_t ngroups = gridDim.x * blockDim.x / G;
+  const uint32_t group = blockIdx.x * gpb + gib;
+  const uint32_t ngroups = gridDim.x * gpb;
   const bool active = 4u * q < a.ld;
   const uint32_t col = 4u * q;
   // Idle lanes (4q >= ld) re-read column 0..3 so every load is unconditional and valid.
   const uint32_t colc = active ? col : 0u;
   const double* __restrict__ fleaf = a.fac[N - 1] + colc;
   // Row-reduction staging ring of this group (D > 0), after all groups' tables.
-  double* rbuf = reinterpret_cast<double*>(smem + (blockDim.x / G) * group_smem_words<N>()) +
+  double* rbuf = reinterpret_cast<double*>(smem + gpb * group_smem_words<N>()) +
                  (size_t)gib * group_red_doubles<D>(a.ld);
   uint32_t rslot = 0, rissued = 0;
   double* hacc = rbuf + kRedBufs * a.ld;  // kHot private rows (D > 0)
@@ -300,6 +318,7 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const uint32_t t = q + e * G;
+        if (G * E > kBatch && t >= (uint32_t)kBatch) break;
         uint32_t w[KW];
 #pragma unroll
         for (int z = 0; z < KW; ++z) w[z] = 0u;
@@ -484,10 +503,11 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
   // groups with many levels); the kernel indexes groups by blockDim, not kBlock.
   int threads = kBlock;
   auto smem_for = [&](int thr) {
-    return (size_t)(thr / G) * (group_smem_words<N>() * 4 + group_red_doubles<D>(ld) * 8);
+    return (size_t)Lanes<G>::groups_per_block(thr) *
+           (group_smem_words<N>() * 4 + group_red_doubles<D>(ld) * 8);
   };
   while (threads > 64 && smem_for(threads) > 160 * 1024) threads /= 2;
-  const int groups_per_block = threads / G;
+  const int groups_per_block = Lanes<G>::groups_per_block(threads);
   const size_t smem = smem_for(threads);
   static bool attr = false;
   if (!attr) {
@@ -522,6 +542,10 @@ void launch_g(splatt_ctx* ctx, DevCsf& c, const double* const* f, double* out, i
   if constexpr (ALLG) {
     if (slots <= 2) return launch_t<N, D, 2, U, MB>(ctx, c, f, out, ld, R, chunk);
     if (slots <= 4) return launch_t<N, D, 4, U, MB>(ctx, c, f, out, ld, R, chunk);
+#ifndef SB_MTTKRP_NO_PACK
+    if (slots == 9 || slots == 10)  // R = 33..40: 3 packed groups per warp
+      return launch_t<N, D, 10, U, MB>(ctx, c, f, out, ld, R, chunk);
+#endif
     if (slots <= 16 && slots > 8) return launch_t<N, D, 16, U, MB>(ctx, c, f, out, ld, R, chunk);
   }
   if (slots <= 8) return launch_t<N, D, 8, U, MB>(ctx, c, f, out, ld, R, chunk);
