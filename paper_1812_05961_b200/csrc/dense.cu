@@ -188,36 +188,55 @@ struct RowsArgs {
 
 constexpr int kRPG = 4;  // rows per lane group per tile
 
-template <int kMaxBP, int G>  // kMaxBP: 1 when there are <= 256 block pairs (ld <= 88), else 3
-__global__ void __launch_bounds__(kThreads, kMaxBP == 1 ? 2 : 1) solve_gram_kernel(const RowsArgs a) {
+// BT threads per CTA; tiles of T = (BT / G) * kRPG rows, double-buffered: the next tile's
+// rows are copied (cp.async) while the current one is solved.
+template <int kMaxBP, int G, int BT>  // kMaxBP: 1 when <= BT block pairs, else 3
+__global__ void __launch_bounds__(BT, kMaxBP == 1 ? (BT == 128 ? 4 : 2) : 1)
+    solve_gram_kernel(const RowsArgs a) {
   extern __shared__ __align__(16) double sm[];
-  __shared__ double red[kThreads];
+  __shared__ double red[BT];
   const int R = a.R, ld = a.ld, ldp = ld + 2, T = a.T;
   const size_t SL = (size_t)R * R + R + 1;
   double* out = a.part + (size_t)blockIdx.x * SL;
   double* Ws = sm;                                   // ld x ld if solve (zero pads)
-  double* tile = Ws + (a.solve ? ld * ld : 0);       // T x ldp
+  const int nb = ld / 4;
+  const int nbp = nb * (nb + 1) / 2;
+  const int S = nbp >= BT ? 1 : BT / nbp;
+  const size_t tile_sz = (size_t)T * ldp;
+  double* tiles = Ws + (a.solve ? ld * ld : 0);      // 2 x T x ldp (+ combine area)
   const bool dead = a.status && *a.status;
   if (a.solve && !dead) {  // Vinv is ld x ld with zero pads: one contiguous async copy
     const unsigned base = (unsigned)__cvta_generic_to_shared(Ws);
     for (int e = threadIdx.x; e < ld * ld / 2; e += blockDim.x)
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(base + 16 * e),
                    "l"(a.Vinv + 2 * e));
-    asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  const int q = threadIdx.x & (G - 1);
+  const double* src = a.solve ? a.M : a.A;
+  const int half = ld / 2;  // 16-byte pairs per row
+  auto load_tile = [&](uint64_t tI, double* buf) {
+    if (tI < a.ntiles && !dead) {
+      const uint64_t row0 = a.lo + tI * T;
+      const uint64_t left = a.hi - row0;
+      const int nrows = left < (uint64_t)T ? (int)left : T;
+      const double* gsrc = src + row0 * ld;
+      for (int e = threadIdx.x; e < nrows * half; e += blockDim.x) {
+        const int r = e / half, c = 2 * (e % half);
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(buf + r * ldp + c);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gsrc + 2 * e));
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const int q = threadIdx.x % G;
   const int grp = threadIdx.x / G;
   const int col = 4 * q;
   const bool active = col < ld;
-  const int nb = ld / 4;
-  const int nbp = nb * (nb + 1) / 2;
-  const int S = nbp >= kThreads ? 1 : kThreads / nbp;
   const int s_id = (S > 1) ? (int)threadIdx.x / nbp : 0;
   int rb[kMaxBP], cb[kMaxBP];
   double g[kMaxBP][16];
 #pragma unroll
   for (int k = 0; k < kMaxBP; ++k) {
-    const int qq = (S > 1) ? (int)threadIdx.x % nbp + k * nbp : (int)threadIdx.x + k * kThreads;
+    const int qq = (S > 1) ? (int)threadIdx.x % nbp + k * nbp : (int)threadIdx.x + k * BT;
     rb[k] = cb[k] = -1;
     if ((S > 1 ? (k == 0 && s_id < S) : qq < nbp)) block_pair(qq, nb, rb[k], cb[k]);
 #pragma unroll
@@ -225,25 +244,18 @@ __global__ void __launch_bounds__(kThreads, kMaxBP == 1 ? 2 : 1) solve_gram_kern
   }
   // column max: thread -> column cm (< CW, CW = pow2 >= R) over row subset cs of CS
   const int CW = R <= 32 ? 32 : (R <= 64 ? 64 : 128);
-  const int CS = kThreads / CW;
+  const int CS = BT / CW;
   const int cm = threadIdx.x % CW, cs = threadIdx.x / CW;
   double cmax = 0.0, inner = 0.0;
-  const double* src = a.solve ? a.M : a.A;
-  for (uint64_t tI = blockIdx.x; tI < a.ntiles && !dead; tI += gridDim.x) {
+  load_tile(blockIdx.x, tiles);
+  int cur = 0;
+  for (uint64_t tI = blockIdx.x; tI < a.ntiles && !dead; tI += gridDim.x, cur ^= 1) {
     const uint64_t row0 = a.lo + tI * T;
     const uint64_t left = a.hi - row0;
     const int nrows = left < (uint64_t)T ? (int)left : T;
-    __syncthreads();
-    {  // async 16-byte copies global -> padded tile (no register staging, all in flight)
-      const int half = ld / 2;  // 16-byte pairs per row
-      const double* gsrc = src + row0 * ld;
-      for (int e = threadIdx.x; e < nrows * half; e += blockDim.x) {
-        const int r = e / half, c = 2 * (e % half);
-        const unsigned dst = (unsigned)__cvta_generic_to_shared(tile + r * ldp + c);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gsrc + 2 * e));
-      }
-      asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-    }
+    double* tile = tiles + cur * tile_sz;
+    load_tile(tI + gridDim.x, tiles + (cur ^ 1) * tile_sz);  // prefetch the next tile
+    asm volatile("cp.async.wait_group 1;" ::: "memory");      // this tile (and Vinv) landed
     __syncthreads();
     if (a.solve) {
       // x[u][0..3] = sum_k m_u[k] Vinv[k][col..col+3] for the group's kRPG rows: each
@@ -304,7 +316,6 @@ __global__ void __launch_bounds__(kThreads, kMaxBP == 1 ? 2 : 1) solve_gram_kern
         }
       }
       __syncthreads();
-      const int half = ld / 2;
       double2* dst = reinterpret_cast<double2*>(a.A + row0 * ld);
       for (int e = threadIdx.x; e < nrows * half; e += blockDim.x)
         dst[e] = *reinterpret_cast<const double2*>(tile + (e / half) * ldp + 2 * (e % half));
@@ -329,9 +340,11 @@ __global__ void __launch_bounds__(kThreads, kMaxBP == 1 ? 2 : 1) solve_gram_kern
     }
     if (cm < R)
       for (int r = cs; r < nrows; r += CS) cmax = fmax(cmax, fabs(tile[r * ldp + cm]));
+    __syncthreads();  // the buffer is refilled by the next iteration's prefetch
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   if (S > 1) {  // combine the row subsets (reuses the tile area)
-    double* comb = tile;
+    double* comb = tiles;
     __syncthreads();
     if (rb[0] >= 0)
       for (int z = 0; z < 16; ++z) comb[((size_t)s_id * nbp + threadIdx.x % nbp) * 16 + z] = g[0][z];
@@ -339,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, kMaxBP == 1 ? 2 : 1) solve_gram_kern
     if ((int)threadIdx.x < nbp) {
       for (int z = 0; z < 16; ++z) {
         double acc = 0.0;
-        for (int s = 0; s < S; ++s) acc += comb[((size_t)s * nbp + threadIdx.x) * 16 + z];
+        for (int s2 = 0; s2 < S; ++s2) acc += comb[((size_t)s2 * nbp + threadIdx.x) * 16 + z];
         g[0][z] = acc;
       }
     } else {
@@ -351,10 +364,10 @@ __global__ void __launch_bounds__(kThreads, kMaxBP == 1 ? 2 : 1) solve_gram_kern
     if (rb[k] < 0) continue;
     for (int i = 0; i < 4; ++i)
       for (int j = 0; j < 4; ++j) {
-        const int r = 4 * rb[k] + i, s = 4 * cb[k] + j;
-        if (r < R && s < R && r <= s) {
-          out[(size_t)r * R + s] = g[k][i * 4 + j];
-          out[(size_t)s * R + r] = g[k][i * 4 + j];
+        const int r = 4 * rb[k] + i, c2 = 4 * cb[k] + j;
+        if (r < R && c2 < R && r <= c2) {
+          out[(size_t)r * R + c2] = g[k][i * 4 + j];
+          out[(size_t)c2 * R + r] = g[k][i * 4 + j];
         }
       }
   }
@@ -503,25 +516,27 @@ void hadamard_inverse(splatt_ctx* ctx, const double* G_all, int N, int n, int R,
 
 namespace {
 
-template <int KB, int G>
+// Block size: 128 threads (4 CTAs/SM) while a CTA's threads cover every 4x4 Gram block pair
+// (ld <= 60), else 256 (and 3 pairs per thread beyond 256 pairs, ld > 88).
+template <int KB, int G, int BT>
 void launch_rows(const RowsArgs& a, int P, size_t smem, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    SB_CUDA(cudaFuncSetAttribute(solve_gram_kernel<KB, G>,
+    SB_CUDA(cudaFuncSetAttribute(solve_gram_kernel<KB, G, BT>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  solve_gram_kernel<KB, G><<<P, kThreads, smem, s>>>(a);
+  solve_gram_kernel<KB, G, BT><<<P, BT, smem, s>>>(a);
 }
 
-template <int KB>
+template <int KB, int BT>
 void launch_rows_g(int G, const RowsArgs& a, int P, size_t smem, cudaStream_t s) {
   switch (G) {
-    case 2: return launch_rows<KB, 2>(a, P, smem, s);
-    case 4: return launch_rows<KB, 4>(a, P, smem, s);
-    case 8: return launch_rows<KB, 8>(a, P, smem, s);
-    case 16: return launch_rows<KB, 16>(a, P, smem, s);
-    default: return launch_rows<KB, 32>(a, P, smem, s);
+    case 2: return launch_rows<KB, 2, BT>(a, P, smem, s);
+    case 4: return launch_rows<KB, 4, BT>(a, P, smem, s);
+    case 8: return launch_rows<KB, 8, BT>(a, P, smem, s);
+    case 16: return launch_rows<KB, 16, BT>(a, P, smem, s);
+    default: return launch_rows<KB, 32, BT>(a, P, smem, s);
   }
 }
 
@@ -542,10 +557,12 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
   const int slots = ld / 4;
   const int G = slots <= 2 ? 2 : slots <= 4 ? 4 : slots <= 8 ? 8 : slots <= 16 ? 16 : 32;
   const int nb = ld / 4, nbp = nb * (nb + 1) / 2;
-  const int S = nbp >= kThreads ? 1 : kThreads / nbp;
-  const int T = (kThreads / G) * kRPG;
-  // the subset-combine buffer aliases the tile
-  const size_t tile_doubles = std::max<size_t>((size_t)T * ldp, (size_t)S * nbp * 16);
+  const int BT = nbp <= 128 ? 128 : 256;
+  const int KB = nbp <= BT ? 1 : 3;
+  const int S = nbp >= BT ? 1 : BT / nbp;
+  const int T = (BT / G) * kRPG;
+  // two tile buffers; the subset-combine buffer aliases them
+  const size_t tile_doubles = std::max<size_t>(2 * (size_t)T * ldp, (size_t)S * nbp * 16);
   const size_t smem = (solve ? (size_t)ld * ld * 8 : 0) + tile_doubles * 8;
   RowsArgs a{};
   a.M = M;
@@ -559,13 +576,16 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
   a.Vinv = Vinv;
   a.status = status;
   a.solve = solve;
-  const int per_sm = std::max<int>(1, std::min<int>(2, (int)((228 * 1024) / (smem + 2048))));
+  const int max_res = KB == 1 ? (BT == 128 ? 4 : 2) : 1;  // __launch_bounds__ residency
+  const int per_sm =
+      std::max<int>(1, std::min<int>(max_res, (int)((228 * 1024) / (smem + 2048))));
   const int P = (int)std::min<uint64_t>(a.ntiles, (uint64_t)ctx->num_sms * per_sm);
   ArenaScope scratch(current_arena() ? ctx->arena_scratch : nullptr, true);  // per-launch
   DevBuf<double> part((size_t)P * SL, s);
   a.part = part.p;
-  if (nbp <= kThreads) launch_rows_g<1>(G, a, P, smem, s);
-  else launch_rows_g<3>(G, a, P, smem, s);
+  if (BT == 128) launch_rows_g<1, 128>(G, a, P, smem, s);
+  else if (KB == 1) launch_rows_g<1, 256>(G, a, P, smem, s);
+  else launch_rows_g<3, 256>(G, a, P, smem, s);
   SB_CHECK_LAUNCH(ctx);
   reduce_stats_kernel<<<(unsigned)ceil_div(SL, kThreads / 32), kThreads, 0, s>>>(part.p, P, R,
                                                                                 stats);
