@@ -220,16 +220,22 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   const double* fac[SPLATT_MAX_NMODES] = {nullptr};
   for (int n = 0; n < N; ++n) fac[n] = A[n].p;
   const size_t RR = (size_t)R * R;
-  DevBuf<double> Gall(N * RR, s), stats(stats_len(R), s), Vinv((size_t)ld * ld, s), lambda(R, s), inner(1, s),
-      M(maxI * ld, s), fit_hist(max_iters, s), nu(R, s);
+  DevBuf<double> Gall(N * RR, s), stats(stats_len(R), s), Vinv((size_t)ld * ld, s), lambda(R, s),
+      inner(1, s), M(maxI * ld, s), fit_hist(max_iters, s), nu(R, s), sig((size_t)N * R, s),
+      tau(R, s);
   DevBuf<int> status(1, s);
+  DevBuf<unsigned> ticket(1, s);
   SB_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int), s));
+  SB_CUDA(cudaMemsetAsync(ticket.p, 0, sizeof(unsigned), s));
+  // The factors stay unnormalised in memory: A_n = stored_n * diag(sig_n);
+  // MTTKRP runs on the stored rows and the solve maps the result back with tau.
+  fill(ctx, sig.p, (size_t)N * R, 1.0);
   SB_CUDA(cudaMemsetAsync(fit_hist.p, 0, max_iters * sizeof(double), s));
   tm.gap();
   tm.begin(kAta);
   for (int n = 0; n < N; ++n) {   // initial Grams (C-4); factors are replicated
-    rows_solve_stats(ctx, nullptr, A[n].p, 0, X.dims[n], R, ld, nullptr, false, false, nullptr,
-                     stats.p);
+    rows_solve_stats(ctx, nullptr, A[n].p, 0, X.dims[n], R, ld, nullptr, nullptr, false, false,
+                     nullptr, stats.p);
     gram_from_stats(ctx, stats.p, R, Gall.p + n * RR);
   }
   tm.end();
@@ -261,7 +267,8 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     }
     if (next >= 0) {
       tma.begin(kInverse);
-      hadamard_inverse(ctx, Gall.p, N, next, R, ld, Vinv.p, status.p, aux);  // lines 4/7/10
+      hadamard_inverse(ctx, Gall.p, N, next, R, ld, Vinv.p, status.p, sig.p, tau.p,
+                       aux);  // lines 4/7/10
       tma.end();
     }
     SB_CUDA(cudaEventRecord(ctx->ev_aux, aux));
@@ -280,9 +287,13 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       }
       SB_CUDA(cudaStreamWaitEvent(s, ctx->ev_aux, 0));  // V^-1 of mode n is ready
       tm.gap();
+      // M V^-1 + statistics; single rank: the reduction kernel also forms lambda, G_n, sig
+      // (line 6); sharded: the statistics are all-reduced first.
+      const LambdaOut lo_fused{it == 1, lambda.p, Gall.p + n * RR, inner.p, sig.p + (size_t)n * R,
+                               ticket.p};
       tm.begin(kInverse);
-      rows_solve_stats(ctx, M.p, A[n].p, lo, hi, R, ld, Vinv.p, true, n == N - 1, status.p,
-                       stats.p);                                           // M V^-1 + stats
+      rows_solve_stats(ctx, M.p, A[n].p, lo, hi, R, ld, Vinv.p, tau.p, true, n == N - 1,
+                       status.p, stats.p, sharded ? nullptr : &lo_fused);
       tm.end();
       if (sharded) {
         tm.begin(kComm);
@@ -290,17 +301,14 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
         ctx->comm->allreduce_max(stats.p + stats_max_off(R), R, s);
         ctx->comm->allgatherv_rows(A[n].p, bounds[n], ld, s);
         tm.end();
+        tm.begin(kNorm);
+        lambda_gram(ctx, stats.p, R, it == 1, lambda.p, Gall.p + n * RR, inner.p,
+                    sig.p + (size_t)n * R);  // line 6
+        tm.end();
       }
-      tm.begin(kNorm);
-      lambda_gram(ctx, stats.p, R, it == 1, lambda.p, Gall.p + n * RR, inner.p);  // line 6
-      tm.end();
       const bool last = (n == N - 1);
       const bool more = !(last && it == max_iters);
       launch_aux(more ? (n + 1) % N : -1, last && fit_on_aux, it);
-      tm.gap();
-      tm.begin(kNorm);
-      scale_columns(ctx, A[n].p, 0, X.dims[n], R, ld, lambda.p);
-      tm.end();
     }
     it_done = it;
     if (!fit_on_aux) {
@@ -326,7 +334,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   // Enqueued before the status is read (one host sync per call end); on SINGULAR the
   // caller's outputs are unspecified.
   for (int n = 0; n < N; ++n) {
-    fold_norms(ctx, Gall.p + n * RR, R, lambda.p, nu.p);
+    fold_norms(ctx, Gall.p + n * RR, R, lambda.p, nu.p, sig.p + (size_t)n * R);
     scale_columns(ctx, A[n].p, 0, X.dims[n], R, ld, nu.p);
     SB_CUDA(cudaMemcpy2DAsync(out.factors[n], R * sizeof(double), A[n].p, ld * sizeof(double),
                               R * sizeof(double), X.dims[n], cudaMemcpyDefault, s));

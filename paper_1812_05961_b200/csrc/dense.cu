@@ -84,7 +84,8 @@ __global__ void sum_partials_kernel(const double* __restrict__ part, int P, doub
 // Vinv, ld x ld (row-major, zero pad rows/columns >= R).  Each step is one parallel pass
 // over the matrix (two barriers), so the kernel is R short steps, not R^2 serial ones.
 __global__ void hadamard_inverse_kernel(const double* __restrict__ G_all, int N, int n, int R,
-                                        int ld, double* __restrict__ Vinv, int* status) {
+                                        int ld, double* __restrict__ Vinv, int* status,
+                                        const double* __restrict__ sig, double* __restrict__ tau) {
   extern __shared__ double sm[];
   double* A = sm;            // R x R working matrix
   double* prow = A + R * R;  // pivot row of the current step (R)
@@ -148,11 +149,23 @@ __global__ void hadamard_inverse_kernel(const double* __restrict__ G_all, int N,
     if (threadIdx.x == 0) *status = 1;
     return;
   }
-  // symmetrise (the elimination rounds the two triangles differently) and pad to ld
+  // tau_i = prod_{m != n} sig_m[i]: the column scale mapping the MTTKRP of the stored
+  // (unnormalised) factors to that of the normalised ones
+  for (int i = threadIdx.x; i < R; i += blockDim.x) {
+    double t = 1.0;
+    if (sig)
+      for (int m = 0; m < N; ++m)
+        if (m != n) t *= sig[(size_t)m * R + i];
+    prow[i] = t;
+    tau[i] = t;
+  }
+  __syncthreads();
+  // symmetrise (the elimination rounds the two triangles differently), scale row i by tau_i
+  // (x = (m o tau) V^-1 = m (diag(tau) V^-1)) and pad to ld
   for (int e = threadIdx.x; e < ld * ld; e += blockDim.x) {
     const int i = e / ld, j = e % ld;
     double v = 0.0;
-    if (i < R && j < R) v = 0.5 * (A[i * R + j] + A[j * R + i]);
+    if (i < R && j < R) v = prow[i] * (0.5 * (A[i * R + j] + A[j * R + i]));
     Vinv[e] = v;
   }
 }
@@ -181,6 +194,7 @@ struct RowsArgs {
   uint64_t lo, hi, ntiles;
   int R, ld, T;
   const double* Vinv;
+  const double* tau;  // R column scales of M (stored -> true MTTKRP), folded into Vinv's rows
   const int* status;
   double* part;  // gridDim.x x stats_len(R)
   bool solve;
@@ -203,7 +217,10 @@ __global__ void __launch_bounds__(BT, kMaxBP == 1 ? (BT == 128 ? 4 : 2) : 1)
   const int nbp = nb * (nb + 1) / 2;
   const int S = nbp >= BT ? 1 : BT / nbp;
   const size_t tile_sz = (size_t)T * ldp;
-  double* tiles = Ws + (a.solve ? ld * ld : 0);      // 2 x T x ldp (+ combine area)
+  double* taus = Ws + (a.solve ? ld * ld : 0);       // ld (solve only)
+  double* tiles = taus + (a.solve ? ld : 0);         // 2 x T x ldp (+ combine area)
+  if (a.solve)
+    for (int r = threadIdx.x; r < ld; r += blockDim.x) taus[r] = (r < R) ? a.tau[r] : 0.0;
   const bool dead = a.status && *a.status;
   if (a.solve && !dead) {  // Vinv is ld x ld with zero pads: one contiguous async copy
     const unsigned base = (unsigned)__cvta_generic_to_shared(Ws);
@@ -303,7 +320,7 @@ __global__ void __launch_bounds__(BT, kMaxBP == 1 ? (BT == 128 ? 4 : 2) : 1)
           if (r0 + u < nrows)
 #pragma unroll
             for (int z = 0; z < 4; ++z)
-              if (col + z < R) inner = fma(m0[u * ldp + col + z], x[u][z], inner);
+              if (col + z < R) inner = fma(m0[u * ldp + col + z] * taus[col + z], x[u][z], inner);
       }
       __syncthreads();  // every group has read its m rows
 #pragma unroll
@@ -387,12 +404,13 @@ __global__ void __launch_bounds__(BT, kMaxBP == 1 ? (BT == 128 ? 4 : 2) : 1)
 
 // stats[e] = fixed-order reduction over P partials: one warp per element, lane l sums
 // partials l, l+32, ... then a fixed shuffle tree (sum; max for the colmax entries).
-__global__ void reduce_stats_kernel(const double* __restrict__ part, int P, int R,
-                                    double* __restrict__ out) {
+__device__ void lambda_gram_body(const double* st, int R, int first, double* lambda, double* G,
+                                 double* inner_out, double* sig, double* lam);
+
+__device__ __forceinline__ void reduce_stats_element(const double* __restrict__ part, int P,
+                                                     int R, double* __restrict__ out, size_t e) {
   const size_t SL = (size_t)R * R + R + 1;
-  const size_t e = blockIdx.x * (size_t)(blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
-  if (e >= SL) return;
   const bool is_max = e > (size_t)R * R;
   double acc = 0.0;
   for (int p = lane; p < P; p += 32) {
@@ -407,30 +425,73 @@ __global__ void reduce_stats_kernel(const double* __restrict__ part, int P, int 
   if (lane == 0) out[e] = acc;
 }
 
-__global__ void lambda_gram_kernel(const double* __restrict__ st, int R, int first,
-                                   double* __restrict__ lambda, double* __restrict__ G,
-                                   double* inner_out) {
+__global__ void reduce_stats_kernel(const double* __restrict__ part, int P, int R,
+                                    double* __restrict__ out) {
+  const size_t SL = (size_t)R * R + R + 1;
+  const size_t e = blockIdx.x * (size_t)(blockDim.x / 32) + threadIdx.x / 32;
+  if (e >= SL) return;
+  reduce_stats_element(part, P, R, out, e);
+}
+
+// reduce_stats_kernel + lambda_gram_kernel in one launch: the last CTA to finish its
+// elements (atomic ticket after a fence) computes lambda / G_n / sig from the reduced
+// statistics.  *ticket must be 0 on entry and is 0 again on exit.
+__global__ void reduce_lambda_kernel(const double* __restrict__ part, int P, int R,
+                                     double* __restrict__ out, int first, double* lambda,
+                                     double* G, double* inner_out, double* sig,
+                                     unsigned* ticket) {
   extern __shared__ double lam[];
+  __shared__ bool last;
+  const size_t SL = (size_t)R * R + R + 1;
+  const size_t e = blockIdx.x * (size_t)(blockDim.x / 32) + threadIdx.x / 32;
+  if (e < SL) reduce_stats_element(part, P, R, out, e);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  lambda_gram_body(out, R, first, lambda, G, inner_out, sig, lam);
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+// a8 + a9 from the reduced statistics: lambda (iteration 1: 2-norm = sqrt(G~_rr); later
+// max(1, colmax)), the normalised Gram G_n = G~ / (lambda lambda^T), the inner product, and
+// the column scale sig_r = 1 / lambda_r (1 for a zero column) that maps the stored,
+// unnormalised rows to the normalised factor (A_n = stored * diag(sig)): the rows are never
+// rescaled in memory.  One CTA; lam: R doubles of shared memory.
+__device__ void lambda_gram_body(const double* st, int R, int first, double* lambda, double* G,
+                                 double* inner_out, double* sig, double* lam) {
   for (int r = threadIdx.x; r < R; r += blockDim.x) {
-    const double l = first ? sqrt(st[(size_t)r * R + r]) : fmax(1.0, st[(size_t)R * R + 1 + r]);
+    // __ldcg: st may have been written by other CTAs of this launch (reduce_lambda_kernel)
+    const double l = first ? sqrt(__ldcg(st + (size_t)r * R + r))
+                           : fmax(1.0, __ldcg(st + (size_t)R * R + 1 + r));
     lam[r] = l;
     lambda[r] = l;
+    if (sig) sig[r] = l > 0.0 ? 1.0 / l : 1.0;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    const int r = e / R, s = e % R;
-    const double u = st[(size_t)min(r, s) * R + max(r, s)];
+    const int r = e / R, c = e % R;
+    const double u = __ldcg(st + (size_t)min(r, c) * R + max(r, c));
     const double lr = lam[r] > 0.0 ? lam[r] : 1.0;
-    const double ls = lam[s] > 0.0 ? lam[s] : 1.0;
-    G[e] = u / (lr * ls);
+    const double lc = lam[c] > 0.0 ? lam[c] : 1.0;
+    G[e] = u / (lr * lc);
   }
-  if (threadIdx.x == 0 && inner_out) inner_out[0] = st[(size_t)R * R];
+  if (threadIdx.x == 0 && inner_out) inner_out[0] = __ldcg(st + (size_t)R * R);
+}
+
+__global__ void lambda_gram_kernel(const double* __restrict__ st, int R, int first,
+                                   double* __restrict__ lambda, double* __restrict__ G,
+                                   double* inner_out, double* sig) {
+  extern __shared__ double lam[];
+  lambda_gram_body(st, R, first, lambda, G, inner_out, sig, lam);
 }
 
 __global__ void gram_from_stats_kernel(const double* __restrict__ st, int R, double* G) {
   for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < R * R; e += blockDim.x * gridDim.x) {
-    const int r = e / R, s = e % R;
-    G[e] = st[(size_t)min(r, s) * R + max(r, s)];
+    const int r = e / R, c = e % R;
+    G[e] = st[(size_t)min(r, c) * R + max(r, c)];
   }
 }
 
@@ -467,13 +528,21 @@ __global__ void fit_kernel(const double* __restrict__ G_all, int N, int R,
   }
 }
 
+// nu_r = ||A_n[:, r]|| of the normalised factor A_n = stored * diag(sig); the output rows
+// are stored / d with d_r = (nu_r > 0 ? nu_r : 1) / sig_r, and lambda_r *= nu_r (C-12).
 __global__ void fold_norms_kernel(const double* __restrict__ G, int R, double* lambda,
-                                  double* nu) {
+                                  double* d, const double* __restrict__ sig) {
   for (int r = threadIdx.x; r < R; r += blockDim.x) {
     const double v = sqrt(G[(size_t)r * R + r]);
-    nu[r] = v;
+    d[r] = (v > 0.0 ? v : 1.0) / (sig ? sig[r] : 1.0);
     if (v > 0.0) lambda[r] *= v;
   }
+}
+
+__global__ void fill_kernel(double* __restrict__ p, size_t n, double v) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n;
+       e += (size_t)gridDim.x * blockDim.x)
+    p[e] = v;
 }
 
 int grid_stride_blocks(splatt_ctx* ctx, uint64_t n) {
@@ -500,7 +569,8 @@ void norm_sq(splatt_ctx* ctx, const double* vals, uint64_t nnz, double* d_out) {
 }
 
 void hadamard_inverse(splatt_ctx* ctx, const double* G_all, int N, int n, int R, int ld,
-                      double* Vinv, int* status, cudaStream_t stream) {
+                      double* Vinv, int* status, const double* sig, double* tau,
+                      cudaStream_t stream) {
   const size_t smem = ((size_t)R * R + 2 * R) * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
@@ -510,7 +580,7 @@ void hadamard_inverse(splatt_ctx* ctx, const double* G_all, int N, int n, int R,
     attr_set = true;
   }
   hadamard_inverse_kernel<<<1, 1024, smem, stream ? stream : ctx->stream>>>(G_all, N, n, R, ld,
-                                                                          Vinv, status);
+                                                                          Vinv, status, sig, tau);
   SB_CHECK_LAUNCH(ctx);
 }
 
@@ -543,8 +613,8 @@ void launch_rows_g(int G, const RowsArgs& a, int P, size_t smem, cudaStream_t s)
 }  // namespace
 
 void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, uint64_t hi,
-                      int R, int ld, const double* Vinv, bool solve, bool inner,
-                      const int* status, double* stats) {
+                      int R, int ld, const double* Vinv, const double* tau, bool solve,
+                      bool inner, const int* status, double* stats, const LambdaOut* fuse) {
   // Vinv: ld x ld, zero pads (hadamard_inverse)
   (void)inner;  // the inner product is always produced by the solve (it is free)
   const size_t SL = stats_len(R);
@@ -563,7 +633,7 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
   const int T = (BT / G) * kRPG;
   // two tile buffers; the subset-combine buffer aliases them
   const size_t tile_doubles = std::max<size_t>(2 * (size_t)T * ldp, (size_t)S * nbp * 16);
-  const size_t smem = (solve ? (size_t)ld * ld * 8 : 0) + tile_doubles * 8;
+  const size_t smem = (solve ? (size_t)ld * ld * 8 + (size_t)ld * 8 : 0) + tile_doubles * 8;
   RowsArgs a{};
   a.M = M;
   a.A = A;
@@ -574,6 +644,7 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
   a.T = T;
   a.ntiles = ceil_div(hi - lo, T);
   a.Vinv = Vinv;
+  a.tau = tau;
   a.status = status;
   a.solve = solve;
   const int max_res = KB == 1 ? (BT == 128 ? 4 : 2) : 1;  // __launch_bounds__ residency
@@ -587,15 +658,21 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
   else if (KB == 1) launch_rows_g<1, 256>(G, a, P, smem, s);
   else launch_rows_g<3, 256>(G, a, P, smem, s);
   SB_CHECK_LAUNCH(ctx);
-  reduce_stats_kernel<<<(unsigned)ceil_div(SL, kThreads / 32), kThreads, 0, s>>>(part.p, P, R,
-                                                                                stats);
+  const unsigned rblocks = (unsigned)ceil_div(SL, kThreads / 32);
+  if (fuse) {
+    reduce_lambda_kernel<<<rblocks, kThreads, R * sizeof(double), s>>>(
+        part.p, P, R, stats, fuse->first ? 1 : 0, fuse->lambda, fuse->G_n, fuse->inner,
+        fuse->sig, fuse->ticket);
+  } else {
+    reduce_stats_kernel<<<rblocks, kThreads, 0, s>>>(part.p, P, R, stats);
+  }
   SB_CHECK_LAUNCH(ctx);
 }
 
 void lambda_gram(splatt_ctx* ctx, const double* stats, int R, bool first, double* lambda,
-                 double* G_n, double* inner_out) {
+                 double* G_n, double* inner_out, double* sig) {
   lambda_gram_kernel<<<1, kThreads, R * sizeof(double), ctx->stream>>>(stats, R, first ? 1 : 0,
-                                                                       lambda, G_n, inner_out);
+                                                                       lambda, G_n, inner_out, sig);
   SB_CHECK_LAUNCH(ctx);
 }
 
@@ -620,8 +697,15 @@ void fit(splatt_ctx* ctx, const double* G_all, int N, int R, const double* lambd
   SB_CHECK_LAUNCH(ctx);
 }
 
-void fold_norms(splatt_ctx* ctx, const double* G_n, int R, double* lambda, double* nu) {
-  fold_norms_kernel<<<1, kThreads, 0, ctx->stream>>>(G_n, R, lambda, nu);
+void fill(splatt_ctx* ctx, double* p, size_t n, double v) {
+  if (!n) return;
+  fill_kernel<<<grid_stride_blocks(ctx, n), kThreads, 0, ctx->stream>>>(p, n, v);
+  SB_CHECK_LAUNCH(ctx);
+}
+
+void fold_norms(splatt_ctx* ctx, const double* G_n, int R, double* lambda, double* d,
+                const double* sig) {
+  fold_norms_kernel<<<1, kThreads, 0, ctx->stream>>>(G_n, R, lambda, d, sig);
   SB_CHECK_LAUNCH(ctx);
 }
 

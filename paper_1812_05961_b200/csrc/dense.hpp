@@ -24,22 +24,43 @@ void norm_sq(splatt_ctx* ctx, const double* vals, uint64_t nnz, double* d_out);
 // pivots squared: the C-7 test (pivot <= 1e-12 * max diag) and one 1e-12*trace/R ridge
 // retry apply as stated.  G_all: N x R*R.  Vinv: ld x ld (symmetric, zero pads).
 // status: set to 1 on failure (never cleared here; Vinv then unwritten).
+// The factors are stored unnormalised: A_m = stored_m * diag(sig_m) (sig: N x R, or NULL =
+// all ones).  The kernel also forms tau = prod_{m != n} sig_m (written to tau, R) and
+// returns Vinv with row i scaled by tau_i, so that x = m_stored Vinv = (m o tau) V^-1.
 // Launched on `stream` (default: the context stream).
 void hadamard_inverse(splatt_ctx* ctx, const double* G_all, int N, int n, int R, int ld,
-                      double* Vinv, int* status, cudaStream_t stream = nullptr);
+                      double* Vinv, int* status, const double* sig, double* tau,
+                      cudaStream_t stream = nullptr);
+
+// Outputs of the lambda step when fused into the statistics reduction (see lambda_gram).
+struct LambdaOut {
+  bool first;
+  double* lambda;   // R
+  double* G_n;      // R x R
+  double* inner;    // 1
+  double* sig;      // R: 1 / lambda (1 for a zero column)
+  unsigned* ticket; // device counter, 0 on entry and on exit
+};
 
 // a7 (solve) + a9/a8/a10 partials: for rows [lo, hi): if solve, A[i,:] = M[i,:] V^-1
 // (row times the symmetric inverse from hadamard_inverse, ld x ld); then accumulate the Gram of
 // the rows, the column max |A| and (if inner) sum M .* A.  Reduced to stats
 // (stats_len(R)).  If !solve, M is ignored and A is only read.  Skipped when *status != 0.
+// tau: R column scales of M (from hadamard_inverse; used for <M, A>), NULL when !solve.
+// fuse: if non-NULL the reduction kernel also performs lambda_gram (single-rank path).
 void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, uint64_t hi,
-                      int R, int ld, const double* Vinv, bool solve, bool inner,
-                      const int* status, double* stats);
+                      int R, int ld, const double* Vinv, const double* tau, bool solve,
+                      bool inner, const int* status, double* stats,
+                      const LambdaOut* fuse = nullptr);
 
 // a8 + a9: lambda (first: 2-norm = sqrt(G~_rr); else max(1, colmax)), G_n =
-// G~ / (lambda lambda^T) (mirrored), inner_out = stats inner.
+// G~ / (lambda lambda^T) (mirrored), inner_out = stats inner, sig = 1 / lambda (the
+// stored rows are not rescaled: A_n = stored * diag(sig)).
 void lambda_gram(splatt_ctx* ctx, const double* stats, int R, bool first, double* lambda,
-                 double* G_n, double* inner_out);
+                 double* G_n, double* inner_out, double* sig);
+
+// p[0..n) = v.
+void fill(splatt_ctx* ctx, double* p, size_t n, double v);
 
 // Mirror the upper Gram of stats into G (R x R) — initial Grams.
 void gram_from_stats(splatt_ctx* ctx, const double* stats, int R, double* G);
@@ -53,7 +74,9 @@ void fit(splatt_ctx* ctx, const double* G_all, int N, int R, const double* lambd
          const double* inner, const double* normx_sq, double* fit_out,
          cudaStream_t stream = nullptr);
 
-// a11 (finalise one mode): nu_r = sqrt(G_n[r,r]); lambda_r *= nu_r; nu written to nu.
-void fold_norms(splatt_ctx* ctx, const double* G_n, int R, double* lambda, double* nu);
+// a11 (finalise one mode): nu_r = sqrt(G_n[r,r]); lambda_r *= nu_r (if > 0); d_r =
+// (nu_r > 0 ? nu_r : 1) / sig_r is the divisor that turns the stored rows into the output.
+void fold_norms(splatt_ctx* ctx, const double* G_n, int R, double* lambda, double* d,
+                const double* sig);
 
 }  // namespace sb
