@@ -218,10 +218,13 @@ splatt_status splatt_csf_build(splatt_ctx* ctx, const splatt_coo* coo, int32_t n
     for (int m = 0; m < nmodes; ++m) c->dims[m] = coo->dims[m];
     int roots[SPLATT_MAX_NMODES];
     csf_policy(nmodes, c->dims, policy, &c->ncsf, roots, c->mode_csf, c->mode_level);
+    DevCsf* outs[SPLATT_MAX_NMODES];
     for (int k = 0; k < c->ncsf; ++k) {
       c->csf[k] = std::make_unique<DevCsf>();
-      build_csf(ctx, X.view.ind, X.view.vals, X.view.nnz, nmodes, X.view.dims, roots[k], *c->csf[k]);
+      outs[k] = c->csf[k].get();
     }
+    build_csf_set(ctx, X.view.ind, X.view.vals, X.view.nnz, nmodes, X.view.dims, roots, c->ncsf,
+                  outs);
     *out = c.release();
   });
 }

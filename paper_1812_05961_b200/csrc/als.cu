@@ -151,10 +151,12 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   std::vector<std::unique_ptr<DevCsf>> csf(std::max(N, ncsf));
   if (!sharded) {
     for (int n = 0; n < N; ++n) bounds[n] = {0, X.dims[n]};
+    DevCsf* outs[SPLATT_MAX_NMODES];
     for (int k = 0; k < ncsf; ++k) {
       csf[k] = std::make_unique<DevCsf>();
-      build_csf(ctx, X.ind, X.vals, X.nnz, N, X.dims, roots[k], *csf[k]);
+      outs[k] = csf[k].get();
     }
+    build_csf_set(ctx, X.ind, X.vals, X.nnz, N, X.dims, roots, ncsf, outs);
   }
   for (int n = 0; n < N && sharded; ++n) {
     csf[n] = std::make_unique<DevCsf>();

@@ -224,26 +224,43 @@ bool validate_coo_device(splatt_ctx* ctx, const uint32_t* const* d_ind, uint64_t
   return h == 0;
 }
 
-void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_vals, uint64_t nnz,
-               int N, const uint64_t* dims, int root, DevCsf& out) {
+namespace {
+
+// The nonzeros of one tree in its lexicographic order: per level the sorted coordinate, and
+// the values.  coord[N-1] and vals become the tree's leaf arrays (finish_levels).
+struct SortedTree {
+  DevBuf<uint32_t> coord[SPLATT_MAX_NMODES];
+  DevBuf<double> vals;
+};
+
+__global__ void iota_kernel(uint32_t* __restrict__ p, uint64_t n) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
+       j += (uint64_t)gridDim.x * blockDim.x)
+    p[j] = (uint32_t)j;
+}
+
+// dst[l][j] = src[l][P[j]] for levels [1, N) and vout[j] = vin[P[j]].
+__global__ void gather_levels_kernel(CoordOut co, uint64_t nnz, const uint32_t* __restrict__ P,
+                                     const double* __restrict__ vin, double* __restrict__ vout) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t q = P[j];
+    for (int l = 1; l < co.N; ++l) co.dst[l][j] = co.src[l][q];
+    vout[j] = vin[q];
+  }
+}
+
+// Full sort of the COO into the order of `perm`: packed composite keys (one or more <= 64-bit
+// groups, LSD), stable radix sort of (key, position), then decode / gather into t (allocated
+// by the caller, alloc_sorted).
+void sort_full(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_vals, uint64_t nnz,
+               int N, const uint64_t* dims, const int* perm, SortedTree& t, PhaseTrace& tr) {
   cudaStream_t st = ctx->stream;
-  PhaseTrace tr(st, "csf_build");
-  // Inside a library call with an arena (cpd_als): temporaries come from the scratch arena,
-  // released when this build returns; the tree itself from the caller's arena.
-  Arena* const out_arena = current_arena();
-  if (out_arena && !ctx->arena_scratch) ctx->arena_scratch = new Arena();
-  ArenaScope scratch(out_arena ? ctx->arena_scratch : nullptr, true);
-  if (nnz >= (1ull << 31)) fail(SPLATT_ERR_UNSUPPORTED, "nnz >= 2^31 not supported");
-  out.N = N;
-  out.nnz = nnz;
-  csf_perm(N, dims, root, out.perm);
   int bits[SPLATT_MAX_NMODES];
   const uint32_t* lvl_src[SPLATT_MAX_NMODES];
-  for (int l = 0; l < N; ++l) out.hot_ready[l] = false;
   for (int l = 0; l < N; ++l) {
-    out.dims[l] = dims[out.perm[l]];
-    bits[l] = bits_for(dims[out.perm[l]]);
-    lvl_src[l] = d_ind[out.perm[l]];
+    bits[l] = bits_for(dims[perm[l]]);
+    lvl_src[l] = d_ind[perm[l]];
   }
   // Key groups, least significant first: levels [lo, hi) with <= 64 bits in total.
   std::vector<std::pair<int, int>> groups;
@@ -256,6 +273,7 @@ void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
     groups.push_back({0, hi});
   }
   const int grid = grid_for(ctx, nnz);
+  ArenaScope tmp_scope(current_arena(), true);  // sort buffers: released on return
   DevBuf<uint64_t> kA(nnz, st), kB(nnz, st);
   DevBuf<uint32_t> pA(nnz, st), pB(nnz, st);
   DevBuf<uint8_t> temp;
@@ -269,9 +287,9 @@ void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
     KeySpec ks{};
     ks.lo = groups[g].first;
     ks.hi = groups[g].second;
-    int sh = 0, total = 0;
+    int sh = 0;
     for (int l = ks.hi - 1; l >= ks.lo; --l) { ks.src[l] = lvl_src[l]; ks.shift[l] = sh; sh += bits[l]; }
-    total = sh;
+    const int total = sh;
     // order == nullptr: first group, positions are the identity (written into pA).
     pack_keys_kernel<<<grid, 256, 0, st>>>(ks, nnz, order, kA.p, pA.p);
     SB_CHECK_LAUNCH(ctx);
@@ -285,29 +303,15 @@ void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
     }
     order = pout;
   }
-  kA.release();
-  temp.release();
   tr.mark("pack+sort");
-
   // Sorted coordinates per level and the permuted values.  With one key group the
   // coordinates are decoded from the sorted keys (sequential reads); otherwise they are
   // gathered through the permutation.
-  DevBuf<uint32_t> coord[SPLATT_MAX_NMODES];
   CoordOut co{};
   co.N = N;
   for (int l = 0; l < N; ++l) {
-    if (l == N - 1) {  // becomes the leaf level of the tree
-      ArenaScope o(out_arena, false);
-      coord[l].alloc(nnz, st);
-    } else {
-      coord[l].alloc(nnz, st);
-    }
     co.src[l] = lvl_src[l];
-    co.dst[l] = coord[l].p;
-  }
-  {
-    ArenaScope o(out_arena, false);
-    out.vals.alloc(nnz, st);
+    co.dst[l] = t.coord[l].p;
   }
   if (groups.size() == 1) {
     KeySpec ks{};
@@ -316,35 +320,47 @@ void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
     for (int l = 0; l < N; ++l) ks.src[l] = nullptr;
     ks.lo = 0;
     ks.hi = N;
-    int maskbits[SPLATT_MAX_NMODES];
-    for (int l = 0; l < N; ++l) maskbits[l] = bits[l];
-    decode_kernel<<<grid, 256, 0, st>>>(ks, BitSet{{maskbits[0], maskbits[1], maskbits[2],
-                                                    maskbits[3], maskbits[4], maskbits[5],
-                                                    maskbits[6], maskbits[7]}},
-                                        co, nnz, kB.p, order, d_vals, out.vals.p);
+    decode_kernel<<<grid, 256, 0, st>>>(ks, BitSet{{bits[0], bits[1], bits[2], bits[3], bits[4],
+                                                    bits[5], bits[6], bits[7]}},
+                                        co, nnz, kB.p, order, d_vals, t.vals.p);
   } else {
-    gather_kernel<<<grid, 256, 0, st>>>(co, nnz, order, d_vals, out.vals.p);
+    gather_kernel<<<grid, 256, 0, st>>>(co, nnz, order, d_vals, t.vals.p);
   }
   SB_CHECK_LAUNCH(ctx);
-  kB.release();
-  pA.release();
-  pB.release();
   tr.mark("decode");
+}
 
-  // Node numbering per internal level.
+// Allocate the sorted-coordinate arrays of a tree: coord[N-1] and vals from `out_arena`
+// (they become the tree's leaf arrays), the rest from the current (scratch) arena.
+void alloc_sorted(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, Arena* out_arena,
+                  bool leaf_to_out) {
+  cudaStream_t st = ctx->stream;
+  for (int l = 0; l < N - 1; ++l) t.coord[l].alloc(nnz, st);
+  ArenaScope o(leaf_to_out ? out_arena : current_arena(), false);
+  t.coord[N - 1].alloc(nnz, st);
+  t.vals.alloc(nnz, st);
+}
+
+// Levels of a tree from its sorted coordinates: "prefix 0..l changed" flags, inclusive scans
+// numbering the nodes, one host sync for the node counts, scatter of ids/ptr.  Moves
+// t.coord[N-1] and t.vals into the tree.
+void finish_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& out,
+                   Arena* out_arena, PhaseTrace& tr) {
+  cudaStream_t st = ctx->stream;
+  const int grid = grid_for(ctx, nnz);
+  ArenaScope tmp_scope(current_arena(), true);
   DevBuf<uint32_t> node[SPLATT_MAX_NMODES];
   FlagOut fo{};
   fo.N = N;
-  for (int l = 0; l < N; ++l) fo.c[l] = coord[l].p;
+  for (int l = 0; l < N; ++l) fo.c[l] = t.coord[l].p;
   for (int l = 0; l < N - 1; ++l) { node[l].alloc(nnz, st); fo.node[l] = node[l].p; }
   level_flags_kernel<<<grid, 256, 0, st>>>(fo, nnz);
   SB_CHECK_LAUNCH(ctx);
-  temp_bytes = 0;
+  size_t temp_bytes = 0;
   SB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, node[0].p, node[0].p, (int)nnz, st));
-  temp.alloc(temp_bytes, st);
+  DevBuf<uint8_t> temp(temp_bytes, st);
   for (int l = 0; l < N - 1; ++l)
     SB_CUDA(cub::DeviceScan::InclusiveSum(temp.p, temp_bytes, node[l].p, node[l].p, (int)nnz, st));
-  temp.release();
   tr.mark("flags+scan");
   std::vector<uint32_t> counts(N, 0);
   for (int l = 0; l < N - 1; ++l)
@@ -359,15 +375,99 @@ void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
       out.ptr[l].alloc(out.nodes[l] + 1, st);
     }
     const uint32_t* child = (l == N - 2) ? nullptr : node[l + 1].p;
-    scatter_level_kernel<<<grid, 256, 0, st>>>(nnz, node[l].p, child, coord[l].p, out.ids[l].p,
-                                               out.ptr[l].p, out.nodes[l], out.nodes[l + 1]);
+    scatter_level_kernel<<<grid, 256, 0, st>>>(nnz, node[l].p, child, t.coord[l].p,
+                                               out.ids[l].p, out.ptr[l].p, out.nodes[l],
+                                               out.nodes[l + 1]);
     SB_CHECK_LAUNCH(ctx);
   }
   tr.mark("scatter");
-  out.ids[N - 1] = std::move(coord[N - 1]);
+  out.ids[N - 1] = std::move(t.coord[N - 1]);
+  out.vals = std::move(t.vals);
   out.tab_chunk = 0;
   out.nchunks = 0;
   out.tab.release();
+}
+
+void init_tree(DevCsf& out, int N, uint64_t nnz, const uint64_t* dims, int root) {
+  out.N = N;
+  out.nnz = nnz;
+  csf_perm(N, dims, root, out.perm);
+  for (int l = 0; l < N; ++l) {
+    out.hot_ready[l] = false;
+    out.dims[l] = dims[out.perm[l]];
+  }
+}
+
+}  // namespace
+
+void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_vals, uint64_t nnz,
+               int N, const uint64_t* dims, int root, DevCsf& out) {
+  DevCsf* o[1] = {&out};
+  build_csf_set(ctx, d_ind, d_vals, nnz, N, dims, &root, 1, o);
+}
+
+void build_csf_set(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_vals,
+                   uint64_t nnz, int N, const uint64_t* dims, const int* roots, int ntrees,
+                   DevCsf* const* outs) {
+  cudaStream_t st = ctx->stream;
+  PhaseTrace tr(st, "csf_build");
+  if (nnz >= (1ull << 31)) fail(SPLATT_ERR_UNSUPPORTED, "nnz >= 2^31 not supported");
+  // Inside a library call with an arena (cpd_als): temporaries come from the scratch arena,
+  // released when this build returns; the trees themselves from the caller's arena.
+  Arena* const out_arena = current_arena();
+  if (out_arena && !ctx->arena_scratch) ctx->arena_scratch = new Arena();
+  ArenaScope scratch(out_arena ? ctx->arena_scratch : nullptr, true);
+  for (int k = 0; k < ntrees; ++k) init_tree(*outs[k], N, nnz, dims, roots[k]);
+  // One full sort, in the order Q of all modes by ascending length (the tree rooted at the
+  // shortest mode).  Every tree rooted at r has level order (r, Q without r), so its order is
+  // a STABLE sort of the Q-ordered nonzeros by their mode-r coordinate alone — a 32-bit key
+  // of ceil(log2 I_r) bits instead of the full composite key.  Ties (equal mode-r
+  // coordinates) keep the Q order, i.e. (Q without r) lexicographically, then input position
+  // for duplicates: bit-identical to sorting each tree's full key.
+  int Q[SPLATT_MAX_NMODES], qlev[SPLATT_MAX_NMODES];
+  csf_perm(N, dims, -1, Q);
+  for (int l = 0; l < N; ++l) qlev[Q[l]] = l;
+  int qtree = -1;
+  for (int k = 0; k < ntrees; ++k)
+    if (roots[k] == Q[0]) qtree = k;
+  SortedTree tq;
+  alloc_sorted(ctx, tq, nnz, N, out_arena, qtree >= 0);
+  sort_full(ctx, d_ind, d_vals, nnz, N, dims, Q, tq, tr);
+  const int grid = grid_for(ctx, nnz);
+  for (int k = 0; k < ntrees; ++k) {
+    if (k == qtree) continue;
+    DevCsf& out = *outs[k];
+    const int r = roots[k];
+    ArenaScope tree_scope(current_arena(), true);
+    SortedTree tr_;
+    alloc_sorted(ctx, tr_, nnz, N, out_arena, true);
+    {
+      ArenaScope sort_scope(current_arena(), true);
+      DevBuf<uint32_t> pos(nnz, st), perm_out(nnz, st);
+      iota_kernel<<<grid, 256, 0, st>>>(pos.p, nnz);
+      SB_CHECK_LAUNCH(ctx);
+      size_t temp_bytes = 0;
+      const int nb = std::max(1, bits_for(dims[r]));
+      SB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, tq.coord[qlev[r]].p,
+                                              tr_.coord[0].p, pos.p, perm_out.p, (int)nnz, 0, nb,
+                                              st));
+      DevBuf<uint8_t> temp(temp_bytes, st);
+      SB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, tq.coord[qlev[r]].p,
+                                              tr_.coord[0].p, pos.p, perm_out.p, (int)nnz, 0, nb,
+                                              st));
+      CoordOut co{};
+      co.N = N;
+      for (int l = 1; l < N; ++l) {
+        co.src[l] = tq.coord[qlev[out.perm[l]]].p;
+        co.dst[l] = tr_.coord[l].p;
+      }
+      gather_levels_kernel<<<grid, 256, 0, st>>>(co, nnz, perm_out.p, tq.vals.p, tr_.vals.p);
+      SB_CHECK_LAUNCH(ctx);
+      tr.mark("derived sort");
+    }
+    finish_levels(ctx, tr_, nnz, N, out, out_arena, tr);
+  }
+  if (qtree >= 0) finish_levels(ctx, tq, nnz, N, *outs[qtree], out_arena, tr);
 }
 
 void ensure_chunk_table(splatt_ctx* ctx, DevCsf& c, int chunk) {

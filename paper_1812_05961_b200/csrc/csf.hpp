@@ -48,6 +48,13 @@ void csf_policy(int N, const uint64_t* dims, int policy, int* ncsf, int* roots, 
 void build_csf(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_vals, uint64_t nnz,
                int N, const uint64_t* dims, int root, DevCsf& out);
 
+// Build the trees rooted at roots[0..ntrees) (distinct modes) from one device COO: one full
+// sort in the ascending-length mode order, every other tree by a short stable re-sort of
+// that order on its root coordinate (csf.cu).  Results are identical to build_csf per root.
+void build_csf_set(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_vals,
+                   uint64_t nnz, int N, const uint64_t* dims, const int* roots, int ntrees,
+                   DevCsf* const* outs);
+
 // Ensure the chunk table for `chunk` leaves per work unit exists.
 void ensure_chunk_table(splatt_ctx* ctx, DevCsf& c, int chunk);
 
