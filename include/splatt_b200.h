@@ -237,6 +237,39 @@ splatt_status splatt_cpd_als_ex(splatt_ctx* ctx, const splatt_coo* coo, int32_t 
                                 const double* const* init_factors, int32_t policy,
                                 splatt_kruskal* out, splatt_stats* stats);
 
+/* ------------------------------------------------------- .tns ingestion and statistics
+ * the paper's datasets are FROSTT .tns files.
+ * Format: one nonzero per line, N 1-based integer indices then a decimal
+ * value, whitespace separated; '#' comment lines and blank lines are skipped; N is the field
+ * count of the first data line minus one (1..8); dims[m] = the largest index seen in mode
+ * m; duplicates are kept in file order.  Host-only (no device needed).                    */
+typedef struct splatt_tensor splatt_tensor;  /* host COO owned by the library           */
+
+/* Parse `path` (multi-threaded, file order preserved) into *out.  Errors: BADINPUT
+ * (unreadable file, no nonzeros, wrong field count, non-integer index, index < 1 or >= 2^32,
+ * non-numeric value: the message, splatt_tensor_error(), names the 1-based line), NOMEM.   */
+splatt_status splatt_tns_read(const char* path, splatt_tensor** out);
+/* A splatt_coo view of t (host pointers into t; valid until splatt_tensor_free).           */
+splatt_status splatt_tensor_coo(const splatt_tensor* t, splatt_coo* view);
+void          splatt_tensor_free(splatt_tensor* t);
+/* Message of the last failed splatt_tns_read / splatt_tns_write on this thread.           */
+const char*   splatt_tensor_error(void);
+/* Write a HOST COO as .tns (1-based; values in shortest round-trip decimal).  nmodes 1..8.  */
+splatt_status splatt_tns_write(const char* path, const splatt_coo* coo);
+
+/* Table I statistics of a HOST COO: dims, nnz, density =
+ * nnz / prod(dims) in floating point, and per mode the non-empty slices and the largest
+ * slice (nonzeros sharing one index).  Errors: BADINPUT (index >= dim, NULL).              */
+typedef struct {
+  int32_t  nmodes;
+  uint64_t nnz;
+  uint64_t dims[SPLATT_MAX_NMODES];
+  double   density;
+  uint64_t nonempty_slices[SPLATT_MAX_NMODES];
+  uint64_t max_slice_nnz[SPLATT_MAX_NMODES];
+} splatt_tensor_stats;
+splatt_status splatt_coo_stats(const splatt_coo* coo, splatt_tensor_stats* out);
+
 #ifdef __cplusplus
 }
 #endif

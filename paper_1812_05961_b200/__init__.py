@@ -20,6 +20,7 @@ import threading
 import numpy as np
 
 __all__ = ["lib", "Context", "Loopback", "Csf", "csf_build", "mttkrp", "cpd_als", "partition",
+           "Tensor", "read_tns", "write_tns", "coo_stats",
            "SplattError", "SingularError", "EmptyTensorError", "STATUS", "padded_ld",
            "CSF_ALL", "CSF_ONE", "CSF_TWO", "POLICIES"]
 
@@ -82,6 +83,19 @@ class Stats(C.Structure):
         return d
 
 
+class TensorStats(C.Structure):
+    _fields_ = [("nmodes", C.c_int32), ("nnz", C.c_uint64), ("dims", C.c_uint64 * MAX_NMODES),
+                ("density", C.c_double), ("nonempty_slices", C.c_uint64 * MAX_NMODES),
+                ("max_slice_nnz", C.c_uint64 * MAX_NMODES)]
+
+    def to_dict(self):
+        n = self.nmodes
+        return dict(nmodes=n, nnz=int(self.nnz), dims=[int(x) for x in self.dims[:n]],
+                    density=float(self.density),
+                    nonempty_slices=[int(x) for x in self.nonempty_slices[:n]],
+                    max_slice_nnz=[int(x) for x in self.max_slice_nnz[:n]])
+
+
 _lib = None
 _lib_lock = threading.Lock()
 
@@ -120,6 +134,12 @@ def lib():
                 "splatt_cpd_als": (st, [P, C.POINTER(Coo), i32, i32, f64, u64, C.POINTER(Kruskal)]),
                 "splatt_cpd_als_ex": (st, [P, C.POINTER(Coo), i32, i32, f64, u64, P, i32,
                                            C.POINTER(Kruskal), C.POINTER(Stats)]),
+                "splatt_tns_read": (st, [C.c_char_p, C.POINTER(P)]),
+                "splatt_tensor_coo": (st, [P, C.POINTER(Coo)]),
+                "splatt_tensor_free": (None, [P]),
+                "splatt_tensor_error": (C.c_char_p, []),
+                "splatt_tns_write": (st, [C.c_char_p, C.POINTER(Coo)]),
+                "splatt_coo_stats": (st, [C.POINTER(Coo), C.POINTER(TensorStats)]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
@@ -439,6 +459,81 @@ def partition(weights, G: int):
     b = np.zeros(G + 1, dtype=np.uint64)
     _raise(lib().splatt_partition(w.ctypes.data if w.size else None, w.shape[0], G, b.ctypes.data))
     return b.astype(np.int64)
+
+
+class Tensor:
+    """A host COO parsed by the library's .tns reader (splatt_tns_read).  ind[m] / vals are
+    zero-copy numpy views of library memory (alive as long as this object)."""
+
+    def __init__(self, path: str):
+        p = C.c_void_p()
+        code = lib().splatt_tns_read(os.fsencode(path), C.byref(p))
+        if code != 0:
+            msg = lib().splatt_tensor_error()
+            cls = {-1: BadInputError}.get(code, SplattError)
+            raise cls(code, (msg.decode() if msg else "") + f" ({path})")
+        self._p = p
+        coo = Coo()
+        _raise(lib().splatt_tensor_coo(p, C.byref(coo)))
+        self.nmodes = int(coo.nmodes)
+        self.nnz = int(coo.nnz)
+        self.dims = tuple(int(coo.dims[m]) for m in range(self.nmodes))
+        self.ind = [np.ctypeslib.as_array(C.cast(coo.ind[m], C.POINTER(C.c_uint32)),
+                                          shape=(self.nnz,)) for m in range(self.nmodes)]
+        self.vals = np.ctypeslib.as_array(C.cast(coo.vals, C.POINTER(C.c_double)),
+                                          shape=(self.nnz,))
+
+    def stats(self) -> dict:
+        return coo_stats(self.ind, self.vals, self.dims)
+
+    def free(self):
+        if getattr(self, "_p", None):
+            self.ind, self.vals = [], None
+            lib().splatt_tensor_free(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def read_tns(path: str) -> Tensor:
+    """splatt_tns_read: parse a FROSTT .tns file (host, multi-threaded)."""
+    return Tensor(path)
+
+
+def _host_coo(ind, vals, dims):
+    ind = [np.ascontiguousarray(np.asarray(a), dtype=np.uint32) for a in ind]
+    vals = np.ascontiguousarray(np.asarray(vals), dtype=np.float64)
+    coo = Coo()
+    coo.nmodes = len(dims)
+    coo.nnz = int(vals.shape[0])
+    for m, d in enumerate(dims):
+        coo.dims[m] = int(d)
+        coo.ind[m] = ind[m].ctypes.data
+    coo.vals = vals.ctypes.data
+    return coo, (ind, vals)
+
+
+def write_tns(path: str, ind, vals, dims) -> None:
+    """splatt_tns_write: host COO -> .tns (1-based, shortest round-trip values)."""
+    coo, keep = _host_coo(ind, vals, dims)
+    code = lib().splatt_tns_write(os.fsencode(path), C.byref(coo))
+    if code != 0:
+        msg = lib().splatt_tensor_error()
+        raise SplattError(code, msg.decode() if msg else "")
+    del keep
+
+
+def coo_stats(ind, vals, dims) -> dict:
+    """splatt_coo_stats: Table I statistics of a host COO."""
+    coo, keep = _host_coo(ind, vals, dims)
+    out = TensorStats()
+    _raise(lib().splatt_coo_stats(C.byref(coo), C.byref(out)))
+    del keep
+    return out.to_dict()
 
 
 def version() -> str:
