@@ -223,7 +223,7 @@ def config_block(cfg, G, policy="all"):
     return {"workload": cfg["name"], "dims": list(cfg["dims"]), "nnz": cfg["nnz"],
             "rank": cfg["rank"], "iters": cfg["iters"], "seed": cfg["seed"],
             "csf_policy": policy,
-            "parallelism": f"slice-partitioned x{G}" if G > 1 else "single GPU",
+            "parallelism": (f"nnz-partitioned x{G} (P2)" if G > 1 else "single GPU"),
             "l2": "inputs larger than L2 (COO + per-mode CSFs >> 126 MB); no explicit flush"}
 
 
@@ -243,6 +243,8 @@ def main():
                     help="seconds between clock samples")
     ap.add_argument("--policy", default="all", choices=["all", "one", "two"],
                     help="CSF allocation policy (SPLATT_CSF_*)")
+    ap.add_argument("--partition", default="nnz", choices=["nnz", "slices"],
+                    help="multi-GPU split: equal nonzero ranges (P2) or whole slices (P1)")
     args = ap.parse_args()
 
     import synth
@@ -275,6 +277,7 @@ def main():
     ctx = sb.Context(local, stream=stream)
     if world > 1:
         ctx.set_comm()
+        ctx.set_partition(args.partition)
 
     N = len(t.dims)
     R, iters = cfg["rank"], cfg["iters"]

@@ -144,6 +144,20 @@ const char*   splatt_version(void);
 splatt_status splatt_comm_unique_id(void* id128);
 splatt_status splatt_ctx_set_comm(splatt_ctx* ctx, const void* id128, int nranks, int rank);
 
+/* How a sharded context splits each mode's nonzeros:
+ *   SLICES (default, P1): contiguous ranges of whole root slices, the optimal cut of C-14
+ *           (splatt_partition); every rank owns the rows of its slices.  Load imbalance is
+ *           bounded by the heaviest slice (power-law tensors: up to 14% of nnz in one slice).
+ *   NNZ (P2, §8(f) NEXT-2): the mode's nonzeros in slice-major order (slices ascending, a
+ *           slice's nonzeros in input order) cut into equal ranges [floor(g nnz/G),
+ *           floor((g+1) nnz/G)); a slice may be split.  Its row belongs to the rank holding
+ *           its first nonzero; the other ranks' partial rows of the <= G-1 split slices are
+ *           summed into it with one all-reduce of (split slices) x ld doubles per mode,
+ *           before the solve.  Results differ from SLICES by rounding only.
+ * Errors: BADINPUT (unknown mode).                                                       */
+enum { SPLATT_PART_SLICES = 0, SPLATT_PART_NNZ = 1 };
+splatt_status splatt_ctx_set_partition(splatt_ctx* ctx, int32_t mode);
+
 /* In-process loopback group (testing/emulation of the sharded path on ONE device): nranks
  * logical ranks, each a host thread with its own context and its own stream (a context
  * on the legacy default stream is rejected), run the same multi-rank ALS as above; the
@@ -159,6 +173,21 @@ void          splatt_loopback_destroy(splatt_loopback* group);
  * boundaries leftmost-greedy under the optimal cap.  bounds: G+1 entries,
  * bounds[0] = 0, bounds[G] = S.  G >= 1.                                          */
 splatt_status splatt_partition(const uint64_t* w, uint64_t S, int32_t G, uint64_t* bounds);
+
+/* Host-only: the SPLATT_PART_NNZ split of slices with nnz weights w[0..S) among G ranks.
+ * row_bounds (G+1): rank g owns rows [row_bounds[g], row_bounds[g+1]); split (G-1
+ * capacity): the split slices, ascending, *nsplit of them; share: rank `rank`'s nonzeros =
+ * whole slices [full_lo, full_hi) plus, for each of npart partial slices, the nonzeros whose
+ * rank within that slice (input order) lies in [part_begin, part_end).  Any output may be
+ * NULL.  Errors: BADINPUT (G < 1, rank out of range, S > 0 with w NULL).               */
+typedef struct {
+  uint64_t full_lo, full_hi;
+  int32_t  npart;
+  uint64_t part_slice[2], part_begin[2], part_end[2];
+} splatt_nnz_share;
+splatt_status splatt_partition_nnz(const uint64_t* w, uint64_t S, int32_t G, int32_t rank,
+                                   uint64_t* row_bounds, uint64_t* split, uint64_t* nsplit,
+                                   splatt_nnz_share* share);
 
 /* ---------------------------------------------------------------- CSF */
 /* Build the CSF set of `coo` on the device (sort = PAPER.md:415).

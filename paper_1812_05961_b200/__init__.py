@@ -123,6 +123,8 @@ def lib():
                 "splatt_ctx_set_comm_loopback": (st, [P, P, i32]),
                 "splatt_loopback_destroy": (None, [P]),
                 "splatt_partition": (st, [P, u64, i32, P]),
+                "splatt_partition_nnz": (st, [P, u64, i32, i32, P, P, P, P]),
+                "splatt_ctx_set_partition": (st, [P, i32]),
                 "splatt_csf_build": (st, [P, C.POINTER(Coo), i32, P, i32, C.POINTER(P)]),
                 "splatt_csf_info": (st, [P, i32, C.POINTER(i32), P, P]),
                 "splatt_csf_export": (st, [P, i32, i32, P, P, P]),
@@ -218,6 +220,11 @@ class Context:
         raw = (C.c_char * 128).from_buffer_copy(obj[0])
         _raise(lib().splatt_ctx_set_comm(self._p, raw, world, rank), self._p)
         self.nranks, self.rank = world, rank
+
+    def set_partition(self, mode: str = "slices"):
+        """How a sharded context splits each mode: "slices" (P1, whole root slices, the
+        C-14 cut) or "nnz" (P2, equal nonzero ranges, split slices exchanged)."""
+        _raise(lib().splatt_ctx_set_partition(self._p, {"slices": 0, "nnz": 1}[mode]), self._p)
 
     def set_comm_loopback(self, group: "Loopback", rank: int):
         """Join an in-process loopback group as logical rank `rank` (testing the sharded
@@ -534,6 +541,27 @@ def coo_stats(ind, vals, dims) -> dict:
     _raise(lib().splatt_coo_stats(C.byref(coo), C.byref(out)))
     del keep
     return out.to_dict()
+
+
+class NnzShare(C.Structure):
+    _fields_ = [("full_lo", C.c_uint64), ("full_hi", C.c_uint64), ("npart", C.c_int32),
+                ("part_slice", C.c_uint64 * 2), ("part_begin", C.c_uint64 * 2),
+                ("part_end", C.c_uint64 * 2)]
+
+
+def partition_nnz(weights, G: int, rank: int):
+    """splatt_partition_nnz (host-only, P2): dict(row_bounds, split, full, parts)."""
+    w = np.ascontiguousarray(np.asarray(weights, dtype=np.uint64))
+    rb = np.zeros(G + 1, dtype=np.uint64)
+    sp = np.zeros(max(1, G - 1), dtype=np.uint64)
+    ns = C.c_uint64()
+    sh = NnzShare()
+    _raise(lib().splatt_partition_nnz(w.ctypes.data if w.size else None, w.shape[0], G, rank,
+                                      rb.ctypes.data, sp.ctypes.data, C.byref(ns), C.byref(sh)))
+    parts = [(int(sh.part_slice[q]), int(sh.part_begin[q]), int(sh.part_end[q]))
+             for q in range(sh.npart)]
+    return dict(row_bounds=rb.astype(np.int64).tolist(), split=sp[: ns.value].astype(np.int64).tolist(),
+                full=(int(sh.full_lo), int(sh.full_hi)), parts=parts)
 
 
 def version() -> str:

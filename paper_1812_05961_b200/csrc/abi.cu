@@ -191,6 +191,34 @@ splatt_status splatt_ctx_set_comm(splatt_ctx* ctx, const void* id128, int nranks
   });
 }
 
+splatt_status splatt_ctx_set_partition(splatt_ctx* ctx, int32_t mode) {
+  if (!ctx || (mode != SPLATT_PART_SLICES && mode != SPLATT_PART_NNZ)) return SPLATT_ERR_BADINPUT;
+  ctx->part_mode = mode;
+  return SPLATT_OK;
+}
+
+splatt_status splatt_partition_nnz(const uint64_t* w, uint64_t S, int32_t G, int32_t rank,
+                                   uint64_t* row_bounds, uint64_t* split, uint64_t* nsplit,
+                                   splatt_nnz_share* share) {
+  if (G < 1 || rank < 0 || rank >= G || (S > 0 && !w)) return SPLATT_ERR_BADINPUT;
+  NnzPart np;
+  host_partition_nnz(w, S, G, rank, np);
+  if (row_bounds) for (int g = 0; g <= G; ++g) row_bounds[g] = np.rowb[g];
+  if (split) for (size_t k = 0; k < np.slots.size(); ++k) split[k] = np.slots[k];
+  if (nsplit) *nsplit = np.slots.size();
+  if (share) {
+    share->full_lo = np.full_lo;
+    share->full_hi = np.full_hi;
+    share->npart = np.npart;
+    for (int q = 0; q < 2; ++q) {
+      share->part_slice[q] = np.pslice[q];
+      share->part_begin[q] = np.pa[q];
+      share->part_end[q] = np.pb[q];
+    }
+  }
+  return SPLATT_OK;
+}
+
 splatt_status splatt_partition(const uint64_t* w, uint64_t S, int32_t G, uint64_t* bounds) {
   if (!bounds || G < 1 || (S > 0 && !w)) return SPLATT_ERR_BADINPUT;
   host_partition(w, S, G, bounds);

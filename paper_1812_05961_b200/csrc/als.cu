@@ -37,6 +37,38 @@ __global__ void owned_flags_kernel(const uint32_t* __restrict__ ind, uint64_t nn
     flag[j] = (ind[j] >= lo && ind[j] < hi) ? 1u : 0u;
 }
 
+__global__ void eq_flags_kernel(const uint32_t* __restrict__ ind, uint64_t nnz, uint32_t v,
+                                uint32_t* __restrict__ flag) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
+       j += (uint64_t)gridDim.x * blockDim.x)
+    flag[j] = (ind[j] == v) ? 1u : 0u;
+}
+
+// P2 share of this rank: whole slices [lo, hi) plus, for up to two partial slices ps[j], the
+// nonzeros whose rank within the slice (input order, rk[j] = exclusive scan of "in slice")
+// lies in [a[j], b[j]).
+struct NnzShare {
+  uint32_t lo, hi;
+  int np;
+  uint32_t ps[2];
+  const uint32_t* rk[2];
+  uint64_t a[2], b[2];
+};
+__global__ void nnz_share_flags_kernel(const uint32_t* __restrict__ ind, uint64_t nnz, NnzShare sh,
+                                       uint32_t* __restrict__ flag) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = ind[j];
+    bool take = (i >= sh.lo && i < sh.hi);
+    for (int q = 0; q < sh.np; ++q)
+      if (i == sh.ps[q]) {
+        const uint64_t r = sh.rk[q][j];
+        take = take || (r >= sh.a[q] && r < sh.b[q]);
+      }
+    flag[j] = take ? 1u : 0u;
+  }
+}
+
 struct Compact {
   const uint32_t* src[SPLATT_MAX_NMODES];
   uint32_t* dst[SPLATT_MAX_NMODES];
@@ -90,6 +122,54 @@ void host_partition(const uint64_t* w, uint64_t S, int G, uint64_t* bounds) {
     bounds[g + 1] = s;
   }
   bounds[G] = S;
+}
+
+void host_partition_nnz(const uint64_t* w, uint64_t S, int G, int me, NnzPart& out) {
+  std::vector<uint64_t> P(S + 1, 0);  // P[s] = position of slice s's first nonzero
+  for (uint64_t t = 0; t < S; ++t) P[t + 1] = P[t] + w[t];
+  const uint64_t nnz = P[S];
+  auto cut = [&](int g) { return (uint64_t)((unsigned __int128)nnz * (unsigned)g / (unsigned)G); };
+  out = NnzPart{};
+  out.rowb.assign(G + 1, S);
+  out.rowb[0] = 0;
+  for (int g = 1; g < G; ++g)  // first slice starting at or after k_g
+    out.rowb[g] = (uint64_t)(std::lower_bound(P.begin(), P.begin() + S, cut(g)) - P.begin());
+  for (int g = 1; g < G; ++g) {  // slices strictly containing a cut (ascending, distinct)
+    const uint64_t k = cut(g);
+    if (k == 0 || k >= nnz) continue;
+    const uint64_t sl = (uint64_t)(std::upper_bound(P.begin(), P.begin() + S + 1, k) - P.begin()) - 1;
+    if (P[sl] < k && (out.slots.empty() || out.slots.back() != sl)) out.slots.push_back(sl);
+  }
+  const uint64_t k0 = cut(me), k1 = cut(me + 1);
+  if (k1 <= k0) { out.full_lo = out.full_hi = 0; return; }
+  // slices holding this rank's first and last nonzero
+  const uint64_t s0 = (uint64_t)(std::upper_bound(P.begin(), P.begin() + S + 1, k0) - P.begin()) - 1;
+  const uint64_t s1 = (uint64_t)(std::upper_bound(P.begin(), P.begin() + S + 1, k1 - 1) - P.begin()) - 1;
+  auto slot_of = [&](uint64_t sl) {
+    for (size_t j = 0; j < out.slots.size(); ++j)
+      if (out.slots[j] == sl) return (int)j;
+    return -1;
+  };
+  out.full_lo = s0;
+  out.full_hi = s1 + 1;
+  const bool first_partial = P[s0] < k0 || P[s0 + 1] > k1;
+  if (first_partial) {
+    out.pslice[out.npart] = s0;
+    out.pa[out.npart] = k0 - P[s0];
+    out.pb[out.npart] = std::min(P[s0 + 1], k1) - P[s0];
+    out.pslot[out.npart] = slot_of(s0);
+    ++out.npart;
+    out.full_lo = s0 + 1;
+  }
+  if (s1 != s0 && P[s1 + 1] > k1) {
+    out.pslice[out.npart] = s1;
+    out.pa[out.npart] = 0;
+    out.pb[out.npart] = k1 - P[s1];
+    out.pslot[out.npart] = slot_of(s1);
+    ++out.npart;
+    out.full_hi = s1;
+  }
+  if (out.full_hi < out.full_lo) out.full_hi = out.full_lo;
 }
 
 void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, double tol,
@@ -148,6 +228,8 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   int ncsf = 0, roots[SPLATT_MAX_NMODES], mode_csf[SPLATT_MAX_NMODES], mode_level[SPLATT_MAX_NMODES];
   csf_policy(N, X.dims, policy, &ncsf, roots, mode_csf, mode_level);
   std::vector<std::vector<uint64_t>> bounds(N);
+  std::vector<NnzPart> nnzpart(N);  // P2 only
+  size_t max_slots = 0;
   std::vector<std::unique_ptr<DevCsf>> csf(std::max(N, ncsf));
   if (!sharded) {
     for (int n = 0; n < N; ++n) bounds[n] = {0, X.dims[n]};
@@ -160,6 +242,10 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   }
   for (int n = 0; n < N && sharded; ++n) {
     csf[n] = std::make_unique<DevCsf>();
+    // this mode's selection / compaction temporaries live in the scratch arena; the local
+    // tree is built into the call arena (build_csf nests its own scratch scope above ours)
+    Arena* const call_arena = current_arena();
+    ArenaScope tmp_scope(call_arena ? ctx->arena_scratch : nullptr, true);
     DevBuf<unsigned long long> cnt(X.dims[n], s);
     SB_CUDA(cudaMemsetAsync(cnt.p, 0, X.dims[n] * 8, s));
     histogram_kernel<<<blocks_for(ctx, X.nnz), 256, 0, s>>>(X.ind[n], X.nnz, cnt.p);
@@ -167,18 +253,48 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     std::vector<uint64_t> hc(X.dims[n]);
     SB_CUDA(cudaMemcpyAsync(hc.data(), cnt.p, X.dims[n] * 8, cudaMemcpyDeviceToHost, s));
     host_sync(ctx);
-    bounds[n].assign(G + 1, 0);
-    host_partition(hc.data(), X.dims[n], G, bounds[n].data());
-    const uint32_t lo = (uint32_t)bounds[n][me], hi = (uint32_t)bounds[n][me + 1];
     DevBuf<uint32_t> flag(X.nnz, s), pos(X.nnz, s);
-    owned_flags_kernel<<<blocks_for(ctx, X.nnz), 256, 0, s>>>(X.ind[n], X.nnz, lo, hi, flag.p);
-    SB_CHECK_LAUNCH(ctx);
+    uint64_t local = 0;
+    std::vector<DevBuf<uint32_t>> rk(2);
+    if (ctx->part_mode == SPLATT_PART_NNZ) {  // P2: equal leaf ranges, slices may split
+      host_partition_nnz(hc.data(), X.dims[n], G, me, nnzpart[n]);
+      const NnzPart& np = nnzpart[n];
+      bounds[n] = np.rowb;
+      NnzShare sh{};
+      sh.lo = (uint32_t)np.full_lo;
+      sh.hi = (uint32_t)np.full_hi;
+      sh.np = np.npart;
+      for (uint64_t i = np.full_lo; i < np.full_hi; ++i) local += hc[i];
+      for (int q = 0; q < np.npart; ++q) {
+        rk[q].alloc(X.nnz, s);
+        eq_flags_kernel<<<blocks_for(ctx, X.nnz), 256, 0, s>>>(X.ind[n], X.nnz,
+                                                               (uint32_t)np.pslice[q], flag.p);
+        SB_CHECK_LAUNCH(ctx);
+        size_t tb = 0;
+        SB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag.p, rk[q].p, (int)X.nnz, s));
+        DevBuf<uint8_t> temp(tb, s);
+        SB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, flag.p, rk[q].p, (int)X.nnz, s));
+        sh.ps[q] = (uint32_t)np.pslice[q];
+        sh.rk[q] = rk[q].p;
+        sh.a[q] = np.pa[q];
+        sh.b[q] = np.pb[q];
+        local += np.pb[q] - np.pa[q];
+      }
+      nnz_share_flags_kernel<<<blocks_for(ctx, X.nnz), 256, 0, s>>>(X.ind[n], X.nnz, sh, flag.p);
+      SB_CHECK_LAUNCH(ctx);
+      max_slots = std::max(max_slots, np.slots.size());
+    } else {  // P1 (C-14): contiguous whole-slice ranges balanced on nnz
+      bounds[n].assign(G + 1, 0);
+      host_partition(hc.data(), X.dims[n], G, bounds[n].data());
+      const uint32_t lo = (uint32_t)bounds[n][me], hi = (uint32_t)bounds[n][me + 1];
+      owned_flags_kernel<<<blocks_for(ctx, X.nnz), 256, 0, s>>>(X.ind[n], X.nnz, lo, hi, flag.p);
+      SB_CHECK_LAUNCH(ctx);
+      for (uint64_t i = lo; i < hi; ++i) local += hc[i];
+    }
     size_t tb = 0;
     SB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag.p, pos.p, (int)X.nnz, s));
     DevBuf<uint8_t> temp(tb, s);
     SB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, flag.p, pos.p, (int)X.nnz, s));
-    uint64_t local = 0;
-    for (uint64_t i = lo; i < hi; ++i) local += hc[i];
     if (local == 0) {  // a rank with no nonzeros of this mode: empty CSF
       csf[n]->N = N;
       csf[n]->nnz = 0;
@@ -197,6 +313,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     SB_CHECK_LAUNCH(ctx);
     const uint32_t* lp[SPLATT_MAX_NMODES];
     for (int m = 0; m < N; ++m) lp[m] = lind[m].p;
+    ArenaScope back(call_arena, false);
     build_csf(ctx, lp, lval.p, local, N, X.dims, n, *csf[n]);
   }
   for (int n = 0; n < N; ++n)  // chunk tables / hot ids before the loop (no syncs inside it)
@@ -227,6 +344,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       tau(R, s);
   DevBuf<int> status(1, s);
   DevBuf<unsigned> ticket(1, s);
+  DevBuf<double> xslots(std::max<size_t>(1, max_slots) * ld, s);  // P2 split-row exchange
   SB_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int), s));
   SB_CUDA(cudaMemsetAsync(ticket.p, 0, sizeof(unsigned), s));
   // The factors stay unnormalised in memory: A_n = stored_n * diag(sig_n);
@@ -286,6 +404,23 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
         ++mttkrp_launches;
       } else {
         SB_CUDA(cudaMemsetAsync(M.p, 0, X.dims[n] * ld * sizeof(double), s));
+      }
+      if (sharded && ctx->part_mode == SPLATT_PART_NNZ && !nnzpart[n].slots.empty()) {
+        // P2: rows of slices split across ranks are summed into their owners' M rows
+        const NnzPart& np = nnzpart[n];
+        const size_t nsl = np.slots.size();
+        tm.gap();
+        tm.begin(kComm);
+        SB_CUDA(cudaMemsetAsync(xslots.p, 0, nsl * ld * sizeof(double), s));
+        for (int q = 0; q < np.npart; ++q)
+          SB_CUDA(cudaMemcpyAsync(xslots.p + (size_t)np.pslot[q] * ld, M.p + np.pslice[q] * ld,
+                                  ld * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        ctx->comm->allreduce_sum(xslots.p, nsl * ld, s);
+        for (size_t k = 0; k < nsl; ++k)
+          if (np.slots[k] >= np.rowb[me] && np.slots[k] < np.rowb[me + 1])
+            SB_CUDA(cudaMemcpyAsync(M.p + np.slots[k] * ld, xslots.p + k * ld, ld * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, s));
+        tm.end();
       }
       SB_CUDA(cudaStreamWaitEvent(s, ctx->ev_aux, 0));  // V^-1 of mode n is ready
       tm.gap();
