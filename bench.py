@@ -243,6 +243,8 @@ def main():
                     help="seconds between clock samples")
     ap.add_argument("--policy", default="all", choices=["all", "one", "two"],
                     help="CSF allocation policy (SPLATT_CSF_*)")
+    ap.add_argument("--leaf-tiling", type=float, default=0.0,
+                    help="ROOT MTTKRP leaf tiling above this fraction of L2 (0 = off)")
     ap.add_argument("--partition", default="nnz", choices=["nnz", "slices"],
                     help="multi-GPU split: equal nonzero ranges (P2) or whole slices (P1)")
     args = ap.parse_args()
@@ -275,6 +277,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     stream = torch.cuda.Stream(local)
     ctx = sb.Context(local, stream=stream)
+    if args.leaf_tiling > 0:
+        ctx.set_leaf_tiling(args.leaf_tiling)
     if world > 1:
         ctx.set_comm()
         ctx.set_partition(args.partition)

@@ -189,6 +189,17 @@ splatt_status splatt_partition_nnz(const uint64_t* w, uint64_t S, int32_t G, int
                                    uint64_t* row_bounds, uint64_t* split, uint64_t* nsplit,
                                    splatt_nnz_share* share);
 
+/* Leaf-mode tiling of the ROOT MTTKRP (the mode tiling the paper's
+ * port omits).  When the leaf factor of a tree (I_leaf x ld doubles)
+ * exceeds l2_fraction x the L2 capacity, the tree is split once (on first use, at the rank
+ * the MTTKRP runs with) into T = ceil(bytes / (l2_fraction x L2)) trees by leaf-id range,
+ * run one after another (later tiles add into the owned rows), so each tile's leaf rows
+ * stay in L2.  It trades DRAM misses for split fibers (more internal-node gathers) and a
+ * one-time split costing about one CSF build: on c3 (480k-row leaf factor, 138 MB) MTTKRP
+ * drops ~6%, so it pays only for long runs.  0 (default) = off.
+ * Errors: BADINPUT (negative or > 4).                                                    */
+splatt_status splatt_ctx_set_leaf_tiling(splatt_ctx* ctx, double l2_fraction);
+
 /* ---------------------------------------------------------------- CSF */
 /* Build the CSF set of `coo` on the device (sort = PAPER.md:415).
  * The policy (SPLATT_CSF_ALL / ONE / TWO above) decides which trees are built: CSF k

@@ -470,6 +470,125 @@ void build_csf_set(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* 
   if (qtree >= 0) finish_levels(ctx, tq, nnz, N, *outs[qtree], out_arena, tr);
 }
 
+namespace {
+
+// flag[ptr[j]] = 1 for the F child-range starts of a level (flag zeroed by the caller).
+__global__ void mark_starts_kernel(const uint32_t* __restrict__ ptr, uint64_t F,
+                                   uint32_t* __restrict__ flag) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < F;
+       j += (uint64_t)gridDim.x * blockDim.x)
+    flag[ptr[j]] = 1u;
+}
+
+// out[k] = table[idx[k] - 1] (idx from an inclusive scan of start flags: 1-based).
+__global__ void gather_minus1_kernel(const uint32_t* __restrict__ table,
+                                     const uint32_t* __restrict__ idx, uint64_t n,
+                                     uint32_t* __restrict__ out) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
+       k += (uint64_t)gridDim.x * blockDim.x)
+    out[k] = table[idx[k] - 1u];
+}
+
+__global__ void tile_key_kernel(const uint32_t* __restrict__ leaf, uint64_t n, uint64_t rows,
+                                uint32_t* __restrict__ key, uint32_t* __restrict__ pos,
+                                unsigned long long* __restrict__ cnt) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = (uint32_t)(leaf[k] / rows);
+    key[k] = t;
+    pos[k] = (uint32_t)k;
+    atomicAdd(&cnt[t], 1ull);
+  }
+}
+
+}  // namespace
+
+void tile_tree(splatt_ctx* ctx, DevCsf& c, int T) {
+  cudaStream_t st = ctx->stream;
+  PhaseTrace tr(st, "tile_tree");
+  const int N = c.N;
+  const uint64_t nnz = c.nnz;
+  const uint64_t rows = (c.dims[N - 1] + T - 1) / T;
+  Arena* const out_arena = current_arena();
+  if (out_arena && !ctx->arena_scratch) ctx->arena_scratch = new Arena();
+  ArenaScope scratch(out_arena ? ctx->arena_scratch : nullptr, true);
+  const int grid = grid_for(ctx, nnz);
+  // 1. per-leaf node index and coordinate of every internal level (start flags + scans)
+  DevBuf<uint32_t> node(nnz, st), lvl[SPLATT_MAX_NMODES], tmp(nnz, st);
+  size_t tb = 0;
+  SB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, tmp.p, tmp.p, (int)nnz, st));
+  DevBuf<uint8_t> temp(tb, st);
+  SB_CUDA(cudaMemsetAsync(node.p, 0, nnz * 4, st));
+  mark_starts_kernel<<<grid, 256, 0, st>>>(c.ptr[N - 2].p, c.nodes[N - 2], node.p);
+  SB_CHECK_LAUNCH(ctx);
+  SB_CUDA(cub::DeviceScan::InclusiveSum(temp.p, tb, node.p, node.p, (int)nnz, st));  // 1-based
+  for (int l = N - 2; l >= 0; --l) {
+    lvl[l].alloc(nnz, st);
+    gather_minus1_kernel<<<grid, 256, 0, st>>>(c.ids[l].p, node.p, nnz, lvl[l].p);
+    SB_CHECK_LAUNCH(ctx);
+    if (l == 0) break;
+    // parent (level l-1) of every level-l node, then of every leaf
+    const uint64_t F = c.nodes[l];
+    DevBuf<uint32_t> par(F, st);
+    SB_CUDA(cudaMemsetAsync(par.p, 0, F * 4, st));
+    mark_starts_kernel<<<grid_for(ctx, c.nodes[l - 1]), 256, 0, st>>>(c.ptr[l - 1].p,
+                                                                      c.nodes[l - 1], par.p);
+    SB_CHECK_LAUNCH(ctx);
+    SB_CUDA(cub::DeviceScan::InclusiveSum(temp.p, tb, par.p, par.p, (int)F, st));
+    gather_minus1_kernel<<<grid, 256, 0, st>>>(par.p, node.p, nnz, tmp.p);  // parent + 1
+    SB_CHECK_LAUNCH(ctx);
+    std::swap(node.p, tmp.p);
+  }
+  // 2. stable order by tile (the tree order inside each tile is kept)
+  DevBuf<uint32_t> key(nnz, st), key2(nnz, st), pos(nnz, st), perm(nnz, st);
+  DevBuf<unsigned long long> cnt(T, st);
+  SB_CUDA(cudaMemsetAsync(cnt.p, 0, T * 8, st));
+  tile_key_kernel<<<grid, 256, 0, st>>>(c.ids[N - 1].p, nnz, rows, key.p, pos.p, cnt.p);
+  SB_CHECK_LAUNCH(ctx);
+  size_t sb = 0;
+  int bits = 1;
+  while ((1 << bits) < T) ++bits;
+  SB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sb, key.p, key2.p, pos.p, perm.p, (int)nnz, 0,
+                                          bits, st));
+  DevBuf<uint8_t> stemp(sb, st);
+  SB_CUDA(cub::DeviceRadixSort::SortPairs(stemp.p, sb, key.p, key2.p, pos.p, perm.p, (int)nnz, 0,
+                                          bits, st));
+  std::vector<unsigned long long> hcnt(T);
+  SB_CUDA(cudaMemcpyAsync(hcnt.data(), cnt.p, T * 8, cudaMemcpyDeviceToHost, st));
+  host_sync(ctx);
+  tr.mark("expand+order");
+  // 3. every tile: gather its coordinates / values (tree order), then its levels
+  c.tiles.clear();
+  uint64_t off = 0;
+  for (int t = 0; t < T; ++t) {
+    const uint64_t n = hcnt[t];
+    if (n == 0) continue;
+    auto tile = std::make_unique<DevCsf>();
+    tile->N = N;
+    tile->nnz = n;
+    for (int l = 0; l < N; ++l) {
+      tile->perm[l] = c.perm[l];
+      tile->dims[l] = c.dims[l];
+      tile->hot_ready[l] = false;
+    }
+    ArenaScope tile_scope(current_arena(), true);
+    SortedTree ts;
+    alloc_sorted(ctx, ts, n, N, out_arena, true);
+    CoordOut co{};
+    co.N = N;
+    for (int l = 0; l < N; ++l) {
+      co.src[l] = (l < N - 1) ? lvl[l].p : c.ids[N - 1].p;
+      co.dst[l] = ts.coord[l].p;
+    }
+    gather_kernel<<<grid_for(ctx, n), 256, 0, st>>>(co, n, perm.p + off, c.vals.p, ts.vals.p);
+    SB_CHECK_LAUNCH(ctx);
+    finish_levels(ctx, ts, n, N, *tile, out_arena, tr);
+    c.tiles.push_back(std::move(tile));
+    off += n;
+  }
+  c.tile_rows = rows;
+}
+
 void ensure_chunk_table(splatt_ctx* ctx, DevCsf& c, int chunk) {
   if (c.tab_chunk == chunk && c.tab.p) return;
   c.nchunks = ceil_div(c.nnz, chunk);

@@ -28,7 +28,15 @@ struct DevCsf {
   // first use of that level as an output level.
   uint32_t hot[SPLATT_MAX_NMODES][8];
   bool hot_ready[SPLATT_MAX_NMODES] = {false};
+  // Leaf-mode tiling for the ROOT MTTKRP: when the leaf factor does
+  // not fit in L2, the same tree split by leaf-id range into tiles (each a tree with the same
+  // level order holding the nonzeros whose leaf id falls in its range), run one after another.
+  std::vector<std::unique_ptr<DevCsf>> tiles;
+  uint64_t tile_rows = 0;  // leaf ids per tile (0 = not tiled)
 };
+
+// Split c by leaf id into T tiles of ceil(I_leaf / T) ids (tiles empty of nonzeros skipped).
+void tile_tree(splatt_ctx* ctx, DevCsf& c, int T);
 
 // perm: root first, then the other modes by ascending length, ties to the lower id
 // (SPEC.md:131).

@@ -16,12 +16,12 @@ namespace sb {
 #endif
 
 void mttkrp_launch_n3(splatt_ctx* ctx, DevCsf& c, int D, const double* const* f, double* out,
-                      int ld, int R, int chunk) {
+                      int ld, int R, int chunk, int acc) {
   constexpr int U = SB_MTTKRP_U, MB = SB_MTTKRP_MINB;
   switch (D) {
-    case 0: return mk::launch_g<3, 0, U, MB, true>(ctx, c, f, out, ld, R, chunk);
-    case 1: return mk::launch_g<3, 1, U, MB, true>(ctx, c, f, out, ld, R, chunk);
-    case 2: return mk::launch_g<3, 2, U, MB, true>(ctx, c, f, out, ld, R, chunk);
+    case 0: return mk::launch_g<3, 0, U, MB, true>(ctx, c, f, out, ld, R, chunk, acc);
+    case 1: return mk::launch_g<3, 1, U, MB, true>(ctx, c, f, out, ld, R, chunk, acc);
+    case 2: return mk::launch_g<3, 2, U, MB, true>(ctx, c, f, out, ld, R, chunk, acc);
     default: fail(SPLATT_ERR_BADINPUT, "level out of range");
   }
 }
@@ -91,8 +91,26 @@ void ensure_hot(splatt_ctx* ctx, DevCsf& c, int level) {
 
 }  // namespace
 
+// Leaf tiles for a ROOT traversal whose leaf factor does not fit in L2 (NEXT-4), when the
+// context enables them (splatt_ctx_set_leaf_tiling): T tiles of at most `leaf_tile_frac` of
+// the L2 capacity each.
+int leaf_tiles(splatt_ctx* ctx, const DevCsf& c, int ld) {
+  const double frac = ctx->leaf_tile_frac;
+  if (!(frac > 0.0)) return 1;
+  const double leaf_bytes = (double)c.dims[c.N - 1] * ld * 8.0;
+  const double budget = frac * (double)(ctx->l2_bytes ? ctx->l2_bytes : (126u << 20));
+  if (leaf_bytes <= budget || c.nnz < (1u << 20)) return 1;
+  return (int)std::min<double>(8.0, std::ceil(leaf_bytes / budget));
+}
+
 void mttkrp_prepare(splatt_ctx* ctx, DevCsf& c, int level, int ld) {
   if (c.nnz == 0) return;
+  if (level == 0) {
+    const int T = leaf_tiles(ctx, c, ld);
+    if (T > 1 && c.tiles.empty()) tile_tree(ctx, c, T);
+    for (auto& t : c.tiles) ensure_chunk_table(ctx, *t, mttkrp_chunk_leaves(c.N, ld));
+    if (!c.tiles.empty()) return;
+  }
   ensure_chunk_table(ctx, c, mttkrp_chunk_leaves(c.N, ld));
   if (level > 0) ensure_hot(ctx, c, level);
 }
@@ -105,13 +123,19 @@ void mttkrp_level(splatt_ctx* ctx, DevCsf& c, int level, const double* const* fa
   SB_CUDA(cudaMemsetAsync(out, 0, out_rows * (size_t)ld * sizeof(double), ctx->stream));
   if (c.nnz == 0) return;
   const int chunk = mttkrp_chunk_leaves(c.N, ld);
-  ensure_chunk_table(ctx, c, chunk);
-  if (level > 0) ensure_hot(ctx, c, level);
+  mttkrp_prepare(ctx, c, level, ld);
+  auto launch = [&](DevCsf& t, int accumulate) {
+    switch (c.N) {
+      case 3: mttkrp_launch_n3(ctx, t, level, fac_by_mode, out, ld, R, chunk, accumulate); break;
+      case 4: mttkrp_launch_n4(ctx, t, level, fac_by_mode, out, ld, R, chunk, accumulate); break;
+      default: mttkrp_launch_nx(ctx, t, level, fac_by_mode, out, ld, R, chunk, accumulate); break;
+    }
+  };
   if (tm) tm->begin(cat);
-  switch (c.N) {
-    case 3: mttkrp_launch_n3(ctx, c, level, fac_by_mode, out, ld, R, chunk); break;
-    case 4: mttkrp_launch_n4(ctx, c, level, fac_by_mode, out, ld, R, chunk); break;
-    default: mttkrp_launch_nx(ctx, c, level, fac_by_mode, out, ld, R, chunk); break;
+  if (level == 0 && !c.tiles.empty()) {
+    for (size_t t = 0; t < c.tiles.size(); ++t) launch(*c.tiles[t], t > 0);
+  } else {
+    launch(c, 0);
   }
   if (tm) tm->end();
 }

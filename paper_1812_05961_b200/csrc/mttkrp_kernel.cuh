@@ -59,6 +59,7 @@ struct Args {
   uint32_t ld;
   int R;
   uint32_t hot[8];            // D > 0: the output level's most frequent ids (~0u = none)
+  int accumulate;             // D = 0: owned rows are added to `out` (later leaf tiles)
 };
 
 struct d4 { double x, y, z, w; };
@@ -400,8 +401,14 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
               }
               if (d <= (uint32_t)D) {
                 if constexpr (D == 0) {
-                  double* dst = (dep[u] & 0x100u) ? a.seam : a.out;
-                  if (active) st_row(dst + (size_t)orow[u] * a.ld + col, mask_pad(acc[0], col, a.R));
+                  const bool seam = dep[u] & 0x100u;
+                  double* dst = (seam ? a.seam : a.out) + (size_t)orow[u] * a.ld + col;
+                  d4 r = mask_pad(acc[0], col, a.R);
+                  if (a.accumulate && !seam && active) {  // a later leaf tile: add to the row
+                    const d4 o = d4{dst[0], dst[1], dst[2], dst[3]};
+                    r = d4{r.x + o.x, r.y + o.y, r.z + o.z, r.w + o.w};
+                  }
+                  if (active) st_row(dst, r);
                 } else {
                   emit_row(orow[u], mask_pad(mul4(acc[D], Q[NP > 0 ? NP - 1 : 0]), col, a.R));
                 }
@@ -479,7 +486,7 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
 
 template <int N, int D, int G, int U, int MINB>
 void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, double* out,
-              int ld, int R, int chunk) {
+              int ld, int R, int chunk, int acc) {
   Args<N> a{};
   for (int l = 0; l < N; ++l) {
     a.ids[l] = c.ids[l].p;
@@ -499,6 +506,7 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
   a.chunk = (uint32_t)chunk;
   a.ld = (uint32_t)ld;
   a.R = R;
+  a.accumulate = acc;
   // 256 threads per block unless the per-group tables would exceed 160 KB (many small
   // groups with many levels); the kernel indexes groups by blockDim, not kBlock.
   int threads = kBlock;
@@ -537,26 +545,29 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
 // for the rarely used N >= 5 (a wider group only idles more lanes).
 template <int N, int D, int U, int MB, bool ALLG>
 void launch_g(splatt_ctx* ctx, DevCsf& c, const double* const* f, double* out, int ld, int R,
-              int chunk) {
+              int chunk, int acc) {
   const int slots = ld / 4;
   if constexpr (ALLG) {
-    if (slots <= 2) return launch_t<N, D, 2, U, MB>(ctx, c, f, out, ld, R, chunk);
-    if (slots <= 4) return launch_t<N, D, 4, U, MB>(ctx, c, f, out, ld, R, chunk);
+    if (slots <= 2) return launch_t<N, D, 2, U, MB>(ctx, c, f, out, ld, R, chunk, acc);
+    if (slots <= 4) return launch_t<N, D, 4, U, MB>(ctx, c, f, out, ld, R, chunk, acc);
 #ifndef SB_MTTKRP_NO_PACK
     if (slots == 9 || slots == 10)  // R = 33..40: 3 packed groups per warp
-      return launch_t<N, D, 10, U, MB>(ctx, c, f, out, ld, R, chunk);
+      return launch_t<N, D, 10, U, MB>(ctx, c, f, out, ld, R, chunk, acc);
 #endif
-    if (slots <= 16 && slots > 8) return launch_t<N, D, 16, U, MB>(ctx, c, f, out, ld, R, chunk);
+    if (slots <= 16 && slots > 8) return launch_t<N, D, 16, U, MB>(ctx, c, f, out, ld, R, chunk, acc);
   }
-  if (slots <= 8) return launch_t<N, D, 8, U, MB>(ctx, c, f, out, ld, R, chunk);
-  return launch_t<N, D, 32, U, MB>(ctx, c, f, out, ld, R, chunk);
+  if (slots <= 8) return launch_t<N, D, 8, U, MB>(ctx, c, f, out, ld, R, chunk, acc);
+  return launch_t<N, D, 32, U, MB>(ctx, c, f, out, ld, R, chunk, acc);
 }
 
 }  // namespace mk
 
 // Per-N entry points (mttkrp.cu / mttkrp_n4.cu / mttkrp_nx.cu): launch the level-D kernel.
-void mttkrp_launch_n3(splatt_ctx*, DevCsf&, int D, const double* const*, double*, int, int, int);
-void mttkrp_launch_n4(splatt_ctx*, DevCsf&, int D, const double* const*, double*, int, int, int);
-void mttkrp_launch_nx(splatt_ctx*, DevCsf&, int D, const double* const*, double*, int, int, int);
+void mttkrp_launch_n3(splatt_ctx*, DevCsf&, int D, const double* const*, double*, int, int, int,
+                      int acc);
+void mttkrp_launch_n4(splatt_ctx*, DevCsf&, int D, const double* const*, double*, int, int, int,
+                      int acc);
+void mttkrp_launch_nx(splatt_ctx*, DevCsf&, int D, const double* const*, double*, int, int, int,
+                      int acc);
 
 }  // namespace sb

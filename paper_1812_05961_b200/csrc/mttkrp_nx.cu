@@ -7,10 +7,10 @@ namespace sb {
 namespace {
 template <int N, int D>
 void go(splatt_ctx* ctx, DevCsf& c, int level, const double* const* f, double* out, int ld,
-        int R, int chunk) {
+        int R, int chunk, int acc) {
   if constexpr (D < N) {
-    if (level == D) return mk::launch_g<N, D, 2, 1, false>(ctx, c, f, out, ld, R, chunk);
-    return go<N, D + 1>(ctx, c, level, f, out, ld, R, chunk);
+    if (level == D) return mk::launch_g<N, D, 2, 1, false>(ctx, c, f, out, ld, R, chunk, acc);
+    return go<N, D + 1>(ctx, c, level, f, out, ld, R, chunk, acc);
   } else {
     fail(SPLATT_ERR_BADINPUT, "level out of range");
   }
@@ -18,12 +18,12 @@ void go(splatt_ctx* ctx, DevCsf& c, int level, const double* const* f, double* o
 }  // namespace
 
 void mttkrp_launch_nx(splatt_ctx* ctx, DevCsf& c, int D, const double* const* f, double* out,
-                      int ld, int R, int chunk) {
+                      int ld, int R, int chunk, int acc) {
   switch (c.N) {
-    case 5: return go<5, 0>(ctx, c, D, f, out, ld, R, chunk);
-    case 6: return go<6, 0>(ctx, c, D, f, out, ld, R, chunk);
-    case 7: return go<7, 0>(ctx, c, D, f, out, ld, R, chunk);
-    case 8: return go<8, 0>(ctx, c, D, f, out, ld, R, chunk);
+    case 5: return go<5, 0>(ctx, c, D, f, out, ld, R, chunk, acc);
+    case 6: return go<6, 0>(ctx, c, D, f, out, ld, R, chunk, acc);
+    case 7: return go<7, 0>(ctx, c, D, f, out, ld, R, chunk, acc);
+    case 8: return go<8, 0>(ctx, c, D, f, out, ld, R, chunk, acc);
     default: fail(SPLATT_ERR_BADINPUT, "nmodes out of range");
   }
 }

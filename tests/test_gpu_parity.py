@@ -267,3 +267,28 @@ def test_errors(sb, ctx):
     with pytest.raises(sb.SingularError):
         sb.cpd_als(ind, vals, t.dims, rank=3, max_iters=1, init=zero, ctx=ctx)
     ctx.sync()  # context still healthy after the errors
+
+
+def test_mttkrp_leaf_tiling(sb, ctx):
+    """NEXT-4: a leaf factor larger than half the L2 (300k rows x 64 doubles = 154 MB) makes the
+    ROOT MTTKRP run on leaf-id tiles (later tiles add into the owned rows); every mode must
+    still match the oracle, and integer inputs bit for bit."""
+    t = synth.generate((60, 50, 300_000), 1_500_000, [("zipf", 1.1), ("uniform",), ("zipf", 1.0)],
+                       "ratings", seed=61)
+    rng = np.random.default_rng(61)
+    R = 64
+    F = [rng.standard_normal((d, R)) for d in t.dims]
+    Fi = [rng.integers(0, 3, (d, R)).astype(np.float64) for d in t.dims]
+    ind, vals = dev_coo(t)
+    ctx = sb.Context(0)
+    ctx.set_leaf_tiling(0.5)
+    csf = sb.csf_build(ind, vals, t.dims, ctx=ctx)
+    fd, fdi = dev_factors(F), dev_factors(Fi)
+    for n in range(3):
+        M = sb.mttkrp(csf, n, fd, rank=R).cpu().numpy()
+        assert rel_fro(M, oracle.mttkrp(t.dims, t.ind, t.vals, F, n)) <= MTTKRP_TOL, n
+        Mi = sb.mttkrp(csf, n, fdi, rank=R).cpu().numpy()
+        assert np.array_equal(Mi, oracle.mttkrp(t.dims, t.ind, t.vals, Fi, n)), n
+    res = sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=2, seed=3, ctx=ctx)
+    ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=R, max_iters=2, seed=3)
+    als_compare(res, ref)
