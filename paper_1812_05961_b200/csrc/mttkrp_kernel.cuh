@@ -158,9 +158,13 @@ struct MetaLayout {
 constexpr int kBatch = 32;
 constexpr int kBlock = 256;
 
+// Per-group table: records + values, plus 4 words of padding so that the tables of the
+// groups sharing a warp start in different 16-byte bank windows (their same-index record
+// and value reads are then conflict-free; without the pad, ncu showed half of the shared
+// wavefronts to be bank conflicts).
 template <int N>
 __host__ __device__ constexpr int group_smem_words() {
-  return MetaLayout<N>::kWords * kBatch + 2 * kBatch;  // meta + values (doubles)
+  return MetaLayout<N>::kWords * kBatch + 2 * kBatch + 4;  // meta + values (doubles) + pad
 }
 
 // INTERNAL / LEAF kernels: output rows are added to global memory with bulk reductions
