@@ -647,7 +647,11 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
   a.tau = tau;
   a.status = status;
   a.solve = solve;
-  const int max_res = KB == 1 ? (BT == 128 ? 4 : 2) : 1;  // __launch_bounds__ residency
+#ifndef SB_SOLVE_MAX_PER_SM
+#define SB_SOLVE_MAX_PER_SM 3
+#endif
+  const int max_res = std::min(SB_SOLVE_MAX_PER_SM,
+                               KB == 1 ? (BT == 128 ? 4 : 2) : 1);  // __launch_bounds__
   const int per_sm =
       std::max<int>(1, std::min<int>(max_res, (int)((228 * 1024) / (smem + 2048))));
   const int P = (int)std::min<uint64_t>(a.ntiles, (uint64_t)ctx->num_sms * per_sm);
