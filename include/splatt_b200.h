@@ -238,7 +238,9 @@ void          splatt_csf_free(splatt_csf* csf);
  * ignored, may be NULL), each dims[m] x ld.  out: device, dims[mode] x ld.
  * Uses the CSF and kernel the build policy assigns to `mode` (splatt_csf_dispatch).
  * ROOT results are deterministic; INTERNAL/LEAF (policies ONE/TWO) accumulate with
- * fp64 atomics, so their rounding order varies run to run.  Errors: BADINPUT (mode,
+ * fp64 atomics, so their rounding order varies run to run.  A CSF set keeps per-tree
+ * MTTKRP scratch (chunk tables, seam rows, hot-row lists, leaf tiles) built on first use:
+ * use a set from one context / stream at a time.  Errors: BADINPUT (mode,
  * rank not in [1,128],
  * ld < rank, NULL pointers).  Asynchronous on the context stream.                  */
 splatt_status splatt_mttkrp(splatt_ctx* ctx, const splatt_csf* csf, int32_t mode,

@@ -572,13 +572,13 @@ void hadamard_inverse(splatt_ctx* ctx, const double* G_all, int N, int n, int R,
                       double* Vinv, int* status, const double* sig, double* tau,
                       cudaStream_t stream) {
   const size_t smem = ((size_t)R * R + 2 * R) * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static const bool attr_set = [] {  // thread-safe one-time init (loopback ranks are threads)
     SB_CUDA(cudaFuncSetAttribute(hadamard_inverse_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (128 * 128 + 2 * 128) * 8));
-    attr_set = true;
-  }
+    return true;
+  }();
+  (void)attr_set;
   hadamard_inverse_kernel<<<1, 1024, smem, stream ? stream : ctx->stream>>>(G_all, N, n, R, ld,
                                                                           Vinv, status, sig, tau);
   SB_CHECK_LAUNCH(ctx);
@@ -590,12 +590,12 @@ namespace {
 // (ld <= 60), else 256 (and 3 pairs per thread beyond 256 pairs, ld > 88).
 template <int KB, int G, int BT>
 void launch_rows(const RowsArgs& a, int P, size_t smem, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static const bool attr = [] {
     SB_CUDA(cudaFuncSetAttribute(solve_gram_kernel<KB, G, BT>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   solve_gram_kernel<KB, G, BT><<<P, BT, smem, s>>>(a);
 }
 

@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
         double v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const uint32_t t = t0 + u;
+          const uint32_t t = min(t0 + u, nb - 1);  // clamped: a U not dividing the batch re-reads the last leaf (its FMA is skipped)
           uint32_t w[KW];
 #pragma unroll
           for (int z = 0; z < MV; ++z) {
@@ -521,22 +521,20 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
   while (threads > 64 && smem_for(threads) > 160 * 1024) threads /= 2;
   const int groups_per_block = Lanes<G>::groups_per_block(threads);
   const size_t smem = smem_for(threads);
-  static bool attr = false;
-  if (!attr) {
+  static const bool attr = [] {  // thread-safe one-time init (loopback ranks are threads)
     SB_CUDA(cudaFuncSetAttribute(mttkrp_csf_kernel<N, D, G, U, MINB>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   uint64_t blocks = ceil_div(c.nchunks, groups_per_block);
   if (D > 0) {
     // persistent grid: each group walks many chunks, so the privatised hot rows are
     // flushed once per group rather than once per chunk
-    static int occ = 0;
-    if (!occ) {
-      SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &occ, mttkrp_csf_kernel<N, D, G, U, MINB>, threads, smem));
-      occ = std::max(occ, 1);
-    }
+    int occ = 0;  // depends on ld through the staging rows' shared memory
+    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ, mttkrp_csf_kernel<N, D, G, U, MINB>, threads, smem));
+    occ = std::max(occ, 1);
     blocks = std::min<uint64_t>(blocks, (uint64_t)ctx->num_sms * occ);
     for (int h = 0; h < 8; ++h) a.hot[h] = c.hot[D][h];
   }
