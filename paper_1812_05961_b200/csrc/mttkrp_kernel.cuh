@@ -179,7 +179,8 @@ constexpr int kRedBufs = 4;  // staging rows per lane group (ring)
 constexpr int kHot = 8;      // privatised hot output rows per lane group
 template <int D>
 __host__ __device__ constexpr int group_red_doubles(int ld) {
-  return D > 0 ? (kRedBufs + kHot) * ld : 0;
+  // + 2 doubles: the groups of a warp start in different 16-byte bank windows (as the tables)
+  return D > 0 ? (kRedBufs + kHot) * ld + 2 : 0;
 }
 
 template <int N, int D, int G, int U, int MINB>
@@ -553,7 +554,7 @@ void launch_g(splatt_ctx* ctx, DevCsf& c, const double* const* f, double* out, i
     if (slots <= 2) return launch_t<N, D, 2, U, MB>(ctx, c, f, out, ld, R, chunk, acc);
     if (slots <= 4) return launch_t<N, D, 4, U, MB>(ctx, c, f, out, ld, R, chunk, acc);
 #ifndef SB_MTTKRP_NO_PACK
-    if (slots == 9 || slots == 10)  // R = 33..40: 3 packed groups per warp
+    if (D == 0 && (slots == 9 || slots == 10))  // ROOT, R = 33..40: 3 packed groups per warp
       return launch_t<N, D, 10, U, MB>(ctx, c, f, out, ld, R, chunk, acc);
 #endif
     if (slots <= 16 && slots > 8) return launch_t<N, D, 16, U, MB>(ctx, c, f, out, ld, R, chunk, acc);
