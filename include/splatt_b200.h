@@ -189,6 +189,15 @@ splatt_status splatt_partition_nnz(const uint64_t* w, uint64_t S, int32_t G, int
                                    uint64_t* row_bounds, uint64_t* split, uint64_t* nsplit,
                                    splatt_nnz_share* share);
 
+/* Bitwise-reproducible ROOT MTTKRP (SURVEY.md §8(b) "Determinism"): a root slice cut by a
+ * chunk seam gets its partial rows added with fp64 atomics by default, so the rounding of
+ * those rows (and of the ALS built on them) can differ run to run.  With `on` the partial rows
+ * are kept per chunk and summed by a second kernel in fixed chunk order; every result of
+ * the ALL policy is then bitwise reproducible (the dense steps already reduce in fixed
+ * order).  INTERNAL/LEAF traversals (ONE/TWO) keep their reductions at L2 and are not
+ * covered.  Costs one small extra kernel per MTTKRP.  Errors: BADINPUT (NULL).         */
+splatt_status splatt_ctx_set_deterministic(splatt_ctx* ctx, int32_t on);
+
 /* Leaf-mode tiling of the ROOT MTTKRP (the mode tiling the paper's
  * port omits).  When the leaf factor of a tree (I_leaf x ld doubles)
  * exceeds l2_fraction x the L2 capacity, the tree is split once (on first use, at the rank

@@ -126,6 +126,7 @@ def lib():
                 "splatt_partition_nnz": (st, [P, u64, i32, i32, P, P, P, P]),
                 "splatt_ctx_set_partition": (st, [P, i32]),
                 "splatt_ctx_set_leaf_tiling": (st, [P, f64]),
+                "splatt_ctx_set_deterministic": (st, [P, i32]),
                 "splatt_csf_build": (st, [P, C.POINTER(Coo), i32, P, i32, C.POINTER(P)]),
                 "splatt_csf_info": (st, [P, i32, C.POINTER(i32), P, P]),
                 "splatt_csf_export": (st, [P, i32, i32, P, P, P]),
@@ -226,6 +227,10 @@ class Context:
         """How a sharded context splits each mode: "slices" (P1, whole root slices, the
         C-14 cut) or "nnz" (P2, equal nonzero ranges, split slices exchanged)."""
         _raise(lib().splatt_ctx_set_partition(self._p, {"slices": 0, "nnz": 1}[mode]), self._p)
+
+    def set_deterministic(self, on: bool = True):
+        """Bitwise-reproducible ROOT MTTKRP (fixed-order chunk-seam sums instead of atomics)."""
+        _raise(lib().splatt_ctx_set_deterministic(self._p, 1 if on else 0), self._p)
 
     def set_leaf_tiling(self, l2_fraction: float = 0.5):
         """Enable ROOT-MTTKRP leaf tiling for leaf factors above l2_fraction x L2 (0 = off)."""

@@ -191,6 +191,12 @@ splatt_status splatt_ctx_set_comm(splatt_ctx* ctx, const void* id128, int nranks
   });
 }
 
+splatt_status splatt_ctx_set_deterministic(splatt_ctx* ctx, int32_t on) {
+  if (!ctx) return SPLATT_ERR_BADINPUT;
+  ctx->deterministic = on != 0;
+  return SPLATT_OK;
+}
+
 splatt_status splatt_ctx_set_leaf_tiling(splatt_ctx* ctx, double l2_fraction) {
   if (!ctx || !(l2_fraction >= 0.0) || l2_fraction > 4.0) return SPLATT_ERR_BADINPUT;
   ctx->leaf_tile_frac = l2_fraction;

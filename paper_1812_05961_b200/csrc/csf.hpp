@@ -23,6 +23,8 @@ struct DevCsf {
   uint64_t nchunks = 0;
   DevBuf<uint32_t> tab;
   DevBuf<double> seam;  // MTTKRP scratch: one row per chunk (chunk-seam slices)
+  DevBuf<double> tail;  // deterministic mode: the open slice's row at each chunk end
+  DevBuf<uint32_t> seamrows;  // deterministic mode: head / tail output rows per chunk
   uint64_t dims[SPLATT_MAX_NMODES] = {0};  // length of the mode at each level
   // Non-root MTTKRP: the 8 most frequent ids of each level (~0u = unused), computed on
   // first use of that level as an output level.

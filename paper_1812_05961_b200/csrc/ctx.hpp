@@ -42,6 +42,7 @@ struct splatt_ctx {
   uint64_t kernel_launches = 0;
   int part_mode = SPLATT_PART_SLICES;  // sharded path: P1 (whole slices) or P2 (equal nnz)
   double leaf_tile_frac = 0.0;         // ROOT MTTKRP leaf tiling (0 = off)
+  bool deterministic = false;          // ROOT MTTKRP seams: fixed-order sums, no atomics
   uint64_t host_syncs = 0;       // blocking stream syncs issued by the library
   double host_sync_s = 0.0;      // host seconds spent in them
   sb::Arena* arena_call = nullptr;       // per-call buffers of cpd_als (see sb::Arena)

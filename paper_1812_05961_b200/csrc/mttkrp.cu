@@ -89,6 +89,29 @@ void ensure_hot(splatt_ctx* ctx, DevCsf& c, int level) {
   c.hot_ready[level] = true;
 }
 
+// Deterministic chunk seams: every chunk whose first slice closed in it (head) sums, in
+// chunk order, the tails of the chunks the slice spans and its own head row into the output
+// row (the only writer of that row).  One warp per chunk, lanes over columns.
+__global__ void seam_combine_kernel(const double* __restrict__ head, const double* __restrict__ tail,
+                                    const uint32_t* __restrict__ headrow,
+                                    const uint32_t* __restrict__ tailrow, uint64_t nchunks, int ld,
+                                    double* __restrict__ out, int accumulate) {
+  const uint64_t c = blockIdx.x * (uint64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (c >= nchunks) return;
+  const uint32_t s = headrow[c];
+  if (s == ~0u) return;
+  uint64_t c0 = c;
+  while (c0 > 0 && tailrow[c0 - 1] == s) --c0;
+  for (int col = lane; col < ld; col += 32) {
+    double acc = 0.0;
+    for (uint64_t k = c0; k < c; ++k) acc += tail[k * ld + col];
+    acc += head[c * ld + col];
+    double* o = out + (size_t)s * ld + col;
+    *o = accumulate ? *o + acc : acc;
+  }
+}
+
 }  // namespace
 
 // Leaf tiles for a ROOT traversal whose leaf factor does not fit in L2 (NEXT-4), when the
@@ -129,6 +152,13 @@ void mttkrp_level(splatt_ctx* ctx, DevCsf& c, int level, const double* const* fa
       case 3: mttkrp_launch_n3(ctx, t, level, fac_by_mode, out, ld, R, chunk, accumulate); break;
       case 4: mttkrp_launch_n4(ctx, t, level, fac_by_mode, out, ld, R, chunk, accumulate); break;
       default: mttkrp_launch_nx(ctx, t, level, fac_by_mode, out, ld, R, chunk, accumulate); break;
+    }
+    if (level == 0 && ctx->deterministic) {
+      const unsigned blocks = (unsigned)ceil_div(t.nchunks, 8);
+      seam_combine_kernel<<<std::max(1u, blocks), 256, 0, ctx->stream>>>(
+          t.seam.p, t.tail.p, t.seamrows.p, t.seamrows.p + t.nchunks, t.nchunks, ld, out,
+          accumulate);
+      SB_CHECK_LAUNCH(ctx);
     }
   };
   if (tm) tm->begin(cat);

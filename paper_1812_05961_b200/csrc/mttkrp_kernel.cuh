@@ -60,6 +60,13 @@ struct Args {
   int R;
   uint32_t hot[8];            // D > 0: the output level's most frequent ids (~0u = none)
   int accumulate;             // D = 0: owned rows are added to `out` (later leaf tiles)
+  // D = 0, deterministic mode (splatt_ctx_set_deterministic): the chunk-seam rows are not
+  // added with atomics but left per chunk (head row in `seam`, tail row in `tail`, their
+  // output rows in headrow / tailrow, ~0u = none) for seam_combine_kernel's fixed-order sum.
+  int det;
+  double* tail;
+  uint32_t* headrow;
+  uint32_t* tailrow;
 };
 
 struct d4 { double x, y, z, w; };
@@ -439,11 +446,15 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
     if constexpr (D == 0) {
       // Chunk seams: the first slice (if it began earlier) and the still-open levels
       // (< last_dep) of the last slice go out through fp64 atomics.
-      if (first_partial && base[0] != slice0 && active) {  // the first slice closed here
+      const bool head = first_partial && base[0] != slice0;  // the first slice closed here
+      if (a.det) {
+        if (q == 0) a.headrow[c] = head ? a.ids[0][slice0] : ~0u;
+      } else if (head && active) {
         const double* sp = a.seam + (size_t)c * a.ld + col;  // written by this same lane
         const d4 r = d4{sp[0], sp[1], sp[2], sp[3]};
         atomic_row(a.out + (size_t)a.ids[0][slice0] * a.ld + col, r);
       }
+      if (a.det && last_dep == 0 && q == 0) a.tailrow[c] = ~0u;
       if (last_dep > 0) {
 #pragma unroll
         for (int l = N - 2; l >= 1; --l) {
@@ -453,8 +464,11 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
             fma4v(acc[l - 1], acc[l], r);
           }
         }
-        if (active) {
-          const uint32_t i = a.ids[0][base[0]];
+        const uint32_t i = a.ids[0][base[0]];
+        if (a.det) {
+          if (active) st_row(a.tail + (size_t)c * a.ld + col, mask_pad(acc[0], col, a.R));
+          if (q == 0) a.tailrow[c] = i;
+        } else if (active) {
           atomic_row(a.out + (size_t)i * a.ld + col, mask_pad(acc[0], col, a.R));
         }
       }
@@ -512,6 +526,14 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
   a.ld = (uint32_t)ld;
   a.R = R;
   a.accumulate = acc;
+  if (D == 0 && ctx->deterministic) {
+    if (c.tail.n < c.nchunks * (size_t)ld) c.tail.alloc(c.nchunks * (size_t)ld, ctx->stream);
+    if (c.seamrows.n < 2 * c.nchunks) c.seamrows.alloc(2 * c.nchunks, ctx->stream);
+    a.det = 1;
+    a.tail = c.tail.p;
+    a.headrow = c.seamrows.p;
+    a.tailrow = c.seamrows.p + c.nchunks;
+  }
   // 256 threads per block unless the per-group tables would exceed 160 KB (many small
   // groups with many levels); the kernel indexes groups by blockDim, not kBlock.
   int threads = kBlock;
