@@ -200,7 +200,10 @@ struct RowsArgs {
   bool solve;
 };
 
-constexpr int kRPG = 4;  // rows per lane group per tile
+#ifndef SB_SOLVE_RPG
+#define SB_SOLVE_RPG 4
+#endif
+constexpr int kRPG = SB_SOLVE_RPG;  // rows per lane group per tile
 
 // BT threads per CTA; tiles of T = (BT / G) * kRPG rows, double-buffered: the next tile's
 // rows are copied (cp.async) while the current one is solved.
