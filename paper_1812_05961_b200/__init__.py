@@ -405,11 +405,26 @@ def mttkrp(csf: Csf, mode: int, factors, out=None, rank: int | None = None,
     (I_mode x ld)."""
     import torch
     ctx = csf.ctx
+    N = len(csf.dims)
+    if not 0 <= mode < N or len(factors) != N:
+        raise ValueError("mode out of range or len(factors) != nmodes")
     ref = next(f for m, f in enumerate(factors) if m != mode and f is not None)
     ld = int(ref.stride(0))
     R = int(rank if rank is not None else ref.shape[1])
+    # the C call reads every factor as dims[m] x ld and writes out as dims[mode] x ld
+    for m, f in enumerate(factors):
+        if m == mode:
+            continue
+        if f is None or not isinstance(f, torch.Tensor) or not f.is_cuda or f.dtype != torch.float64:
+            raise TypeError(f"factors[{m}] must be a float64 CUDA tensor")
+        if f.dim() != 2 or f.shape[0] != csf.dims[m] or f.stride(1) != 1 or f.stride(0) != ld \
+                or f.shape[1] < R:
+            raise ValueError(f"factors[{m}] must be dims[{m}] x >= rank, row stride {ld}")
     if out is None:
         out = torch.empty((csf.dims[mode], ld), dtype=torch.float64, device=ref.device)
+    elif (not out.is_cuda or out.dtype != torch.float64 or out.dim() != 2 or out.stride(1) != 1
+          or out.stride(0) != ld or out.shape[0] != csf.dims[mode]):
+        raise ValueError(f"out must be a float64 CUDA tensor dims[mode] x ld with row stride {ld}")
     arr = (C.c_void_p * len(factors))(*[(_ptr(f) if f is not None and m != mode else None)
                                         for m, f in enumerate(factors)])
     if which is None:
@@ -457,6 +472,11 @@ def cpd_als(ind, vals, dims, rank: int, max_iters: int, tol: float = 0.0, seed: 
     if init is not None:
         init = [np.ascontiguousarray(a, dtype=np.float64) if isinstance(a, np.ndarray)
                 else a.contiguous() for a in init]
+        if len(init) != N or any(tuple(a.shape) != (int(d), rank) for a, d in zip(init, dims)):
+            raise ValueError("init factors must be N arrays of shape (I_n, rank)")
+        if any(not isinstance(a, np.ndarray) and a.dtype != __import__("torch").float64
+               for a in init):
+            raise TypeError("init factors must be float64")
         init_arr = (C.c_void_p * N)(*[_ptr(a) for a in init])
     st = Stats() if stats else None
     code = lib().splatt_cpd_als_ex(ctx.ptr, C.byref(coo), rank, max_iters, float(tol), int(seed),
