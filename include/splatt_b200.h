@@ -321,6 +321,17 @@ typedef struct {
 } splatt_tensor_stats;
 splatt_status splatt_coo_stats(const splatt_coo* coo, splatt_tensor_stats* out);
 
+/* ------------------------------------------------------- CP-ALS on a prebuilt CSF set
+ * As splatt_cpd_als_ex, on the trees of a splatt_csf_build result (its policy decides the
+ * kernels): the build ("Sort") and the COO validation are skipped, so repeated runs on one
+ * tensor (rank sweeps, restarts with other seeds) pay for them once.  ||X||^2 is summed over
+ * the tree's leaf values (another order than the COO's: rounding-level difference).  Not
+ * with a sharded context (UNSUPPORTED).  Errors: as splatt_cpd_als_ex.                  */
+splatt_status splatt_cpd_als_csf(splatt_ctx* ctx, const splatt_csf* csf, int32_t rank,
+                                 int32_t max_iters, double tol, uint64_t seed,
+                                 const double* const* init_factors, splatt_kruskal* out,
+                                 splatt_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,7 +19,8 @@ import threading
 
 import numpy as np
 
-__all__ = ["lib", "Context", "Loopback", "Csf", "csf_build", "mttkrp", "cpd_als", "partition",
+__all__ = ["lib", "Context", "Loopback", "Csf", "csf_build", "mttkrp", "cpd_als", "cpd_als_csf",
+           "partition",
            "Tensor", "read_tns", "write_tns", "coo_stats",
            "SplattError", "SingularError", "EmptyTensorError", "STATUS", "padded_ld",
            "CSF_ALL", "CSF_ONE", "CSF_TWO", "POLICIES"]
@@ -138,6 +139,8 @@ def lib():
                 "splatt_cpd_als": (st, [P, C.POINTER(Coo), i32, i32, f64, u64, C.POINTER(Kruskal)]),
                 "splatt_cpd_als_ex": (st, [P, C.POINTER(Coo), i32, i32, f64, u64, P, i32,
                                            C.POINTER(Kruskal), C.POINTER(Stats)]),
+                "splatt_cpd_als_csf": (st, [P, P, i32, i32, f64, u64, P, C.POINTER(Kruskal),
+                                            C.POINTER(Stats)]),
                 "splatt_tns_read": (st, [C.c_char_p, C.POINTER(P)]),
                 "splatt_tensor_coo": (st, [P, C.POINTER(Coo)]),
                 "splatt_tensor_free": (None, [P]),
@@ -436,19 +439,10 @@ def mttkrp(csf: Csf, mode: int, factors, out=None, rank: int | None = None,
     return out
 
 
-def cpd_als(ind, vals, dims, rank: int, max_iters: int, tol: float = 0.0, seed: int = 0,
-            init=None, ctx: Context | None = None, out_device: bool = True, stats: bool = False,
-            out=None, policy=CSF_ALL):
-    """splatt_cpd_als(_ex).  Returns dict(factors, lam, fit, iters, fit_history[, stats]).
-
-    ind/vals may be host (numpy / CPU tensors) or CUDA tensors; outputs are CUDA
-    tensors if out_device else numpy arrays."""
+def _als_call(dims, rank, max_iters, init, ctx, out_device, stats, out, call):
+    """Output buffers, initial factors and result dict shared by cpd_als / cpd_als_csf;
+    `call(kr, init_arr, st)` performs the C call and returns its status."""
     import torch
-    ctx = ctx or default_context()
-    ind = [_as_u32(a) if not (hasattr(a, "is_cuda") and not a.is_cuda) else _as_u32(a.numpy())
-           for a in ind]
-    vals = _as_f64(vals.numpy() if hasattr(vals, "is_cuda") and not vals.is_cuda else vals)
-    coo = _make_coo(ind, vals, dims)
     N = len(dims)
     if out is not None:  # caller buffers (host — e.g. pinned — or device), ld = rank
         fac, lam = list(out["factors"]), out["lam"]
@@ -474,20 +468,47 @@ def cpd_als(ind, vals, dims, rank: int, max_iters: int, tol: float = 0.0, seed: 
                 else a.contiguous() for a in init]
         if len(init) != N or any(tuple(a.shape) != (int(d), rank) for a, d in zip(init, dims)):
             raise ValueError("init factors must be N arrays of shape (I_n, rank)")
-        if any(not isinstance(a, np.ndarray) and a.dtype != __import__("torch").float64
-               for a in init):
+        if any(not isinstance(a, np.ndarray) and a.dtype != torch.float64 for a in init):
             raise TypeError("init factors must be float64")
         init_arr = (C.c_void_p * N)(*[_ptr(a) for a in init])
     st = Stats() if stats else None
-    code = lib().splatt_cpd_als_ex(ctx.ptr, C.byref(coo), rank, max_iters, float(tol), int(seed),
-                                   init_arr, _policy(policy), C.byref(kr),
-                                   C.byref(st) if st else None)
-    _raise(code, ctx.ptr)
+    _raise(call(kr, init_arr, st), ctx.ptr)
     res = dict(factors=fac, lam=lam, fit=kr.fit, iters=kr.iters,
                fit_history=hist[: kr.iters].copy())
     if st is not None:
         res["stats"] = st.to_dict(N)
     return res
+
+
+def cpd_als(ind, vals, dims, rank: int, max_iters: int, tol: float = 0.0, seed: int = 0,
+            init=None, ctx: Context | None = None, out_device: bool = True, stats: bool = False,
+            out=None, policy=CSF_ALL):
+    """splatt_cpd_als(_ex).  Returns dict(factors, lam, fit, iters, fit_history[, stats]).
+
+    ind/vals may be host (numpy / CPU tensors) or CUDA tensors; outputs are CUDA
+    tensors if out_device else numpy arrays."""
+    ctx = ctx or default_context()
+    ind = [_as_u32(a) if not (hasattr(a, "is_cuda") and not a.is_cuda) else _as_u32(a.numpy())
+           for a in ind]
+    vals = _as_f64(vals.numpy() if hasattr(vals, "is_cuda") and not vals.is_cuda else vals)
+    coo = _make_coo(ind, vals, dims)
+
+    def call(kr, init_arr, st):
+        return lib().splatt_cpd_als_ex(ctx.ptr, C.byref(coo), rank, max_iters, float(tol),
+                                       int(seed), init_arr, _policy(policy), C.byref(kr),
+                                       C.byref(st) if st else None)
+    return _als_call(dims, rank, max_iters, init, ctx, out_device, stats, out, call)
+
+
+def cpd_als_csf(csf: Csf, rank: int, max_iters: int, tol: float = 0.0, seed: int = 0,
+                init=None, out_device: bool = True, stats: bool = False, out=None):
+    """splatt_cpd_als_csf: CP-ALS on a prebuilt CSF set (no build / validation per call)."""
+    ctx = csf.ctx
+
+    def call(kr, init_arr, st):
+        return lib().splatt_cpd_als_csf(ctx.ptr, csf._p, rank, max_iters, float(tol), int(seed),
+                                        init_arr, C.byref(kr), C.byref(st) if st else None)
+    return _als_call(csf.dims, rank, max_iters, init, ctx, out_device, stats, out, call)
 
 
 def partition(weights, G: int):

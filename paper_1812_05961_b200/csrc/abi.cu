@@ -419,6 +419,38 @@ splatt_status splatt_cpd_als_ex(splatt_ctx* ctx, const splatt_coo* coo, int32_t 
   });
 }
 
+splatt_status splatt_cpd_als_csf(splatt_ctx* ctx, const splatt_csf* csf, int32_t rank,
+                                 int32_t max_iters, double tol, uint64_t seed,
+                                 const double* const* init_factors, splatt_kruskal* out,
+                                 splatt_stats* stats) {
+  if (!ctx) return SPLATT_ERR_BADINPUT;
+  return guard(ctx, [&] {
+    SB_REQUIRE(csf != nullptr && csf->ncsf >= 1, "NULL CSF");
+    SB_REQUIRE(rank >= 1 && rank <= SPLATT_MAX_RANK, "rank must be in [1, 128]");
+    SB_REQUIRE(max_iters >= 1, "max_iters must be >= 1");
+    SB_REQUIRE(tol >= 0.0, "tol must be >= 0");
+    SB_REQUIRE(out != nullptr && out->lambda != nullptr, "NULL output");
+    for (int m = 0; m < csf->N; ++m) SB_REQUIRE(out->factors[m] != nullptr, "NULL factor out");
+    if (init_factors)
+      for (int m = 0; m < csf->N; ++m) SB_REQUIRE(init_factors[m] != nullptr, "NULL init");
+    if (ctx->comm)
+      fail(SPLATT_ERR_UNSUPPORTED, "a prebuilt CSF set runs on an unsharded context only");
+    SB_CUDA(cudaSetDevice(ctx->device));
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    DevCoo X;
+    X.N = csf->N;
+    X.nnz = csf->csf[0]->nnz;
+    for (int m = 0; m < csf->N; ++m) X.dims[m] = csf->dims[m];
+    AlsOut o{};
+    for (int m = 0; m < csf->N; ++m) o.factors[m] = out->factors[m];
+    o.lambda = out->lambda;
+    o.fit = &out->fit;
+    o.iters = &out->iters;
+    o.fit_history = out->fit_history;
+    cpd_als_device(ctx, X, rank, max_iters, tol, seed, init_factors, csf->policy, o, stats, csf);
+  });
+}
+
 splatt_status splatt_cpd_als(splatt_ctx* ctx, const splatt_coo* coo, int32_t rank,
                              int32_t max_iters, double tol, uint64_t seed, splatt_kruskal* out) {
   return splatt_cpd_als_ex(ctx, coo, rank, max_iters, tol, seed, nullptr, SPLATT_CSF_ALL, out,

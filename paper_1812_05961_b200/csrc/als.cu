@@ -174,7 +174,7 @@ void host_partition_nnz(const uint64_t* w, uint64_t S, int G, int me, NnzPart& o
 
 void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, double tol,
                     uint64_t seed, const double* const* init, int policy, const AlsOut& out,
-                    splatt_stats* st) {
+                    splatt_stats* st, const splatt_csf* prebuilt) {
   cudaStream_t s = ctx->stream;
   const int N = X.N;
   const int ld = padded_ld(R);
@@ -208,9 +208,12 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   tm.begin(kBuild);
   PhaseTrace tr(s, "cpd_als");
   DevBuf<int> bad(1, s);
-  validate_coo_enqueue(ctx, X.ind, X.nnz, N, X.dims, bad.p);
+  SB_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+  if (!prebuilt) validate_coo_enqueue(ctx, X.ind, X.nnz, N, X.dims, bad.p);
   DevBuf<double> normx(1, s);
-  norm_sq(ctx, X.vals, X.nnz, normx.p);
+  // ||X||^2 from the COO values, or from the leaf values of a prebuilt tree (the same
+  // numbers in another order: the sum differs by rounding only)
+  norm_sq(ctx, prebuilt ? prebuilt->csf[0]->vals.p : X.vals, X.nnz, normx.p);
   double h_normx = 0.0;
   int h_bad = 0;
   SB_CUDA(cudaMemcpyAsync(&h_normx, normx.p, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -226,22 +229,34 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   if (sharded && policy != SPLATT_CSF_ALL)
     fail(SPLATT_ERR_UNSUPPORTED, "a sharded context requires policy ALL");
   int ncsf = 0, roots[SPLATT_MAX_NMODES], mode_csf[SPLATT_MAX_NMODES], mode_level[SPLATT_MAX_NMODES];
-  csf_policy(N, X.dims, policy, &ncsf, roots, mode_csf, mode_level);
+  if (prebuilt) {
+    ncsf = prebuilt->ncsf;
+    for (int n = 0; n < N; ++n) {
+      mode_csf[n] = prebuilt->mode_csf[n];
+      mode_level[n] = prebuilt->mode_level[n];
+    }
+  } else {
+    csf_policy(N, X.dims, policy, &ncsf, roots, mode_csf, mode_level);
+  }
   std::vector<std::vector<uint64_t>> bounds(N);
   std::vector<NnzPart> nnzpart(N);  // P2 only
   size_t max_slots = 0;
-  std::vector<std::unique_ptr<DevCsf>> csf(std::max(N, ncsf));
-  if (!sharded) {
+  std::vector<std::unique_ptr<DevCsf>> owned(std::max(N, ncsf));  // trees built by this call
+  std::vector<DevCsf*> csf(std::max(N, ncsf), nullptr);
+  if (prebuilt) {
     for (int n = 0; n < N; ++n) bounds[n] = {0, X.dims[n]};
-    DevCsf* outs[SPLATT_MAX_NMODES];
+    for (int k = 0; k < ncsf; ++k) csf[k] = prebuilt->csf[k].get();
+  } else if (!sharded) {
+    for (int n = 0; n < N; ++n) bounds[n] = {0, X.dims[n]};
     for (int k = 0; k < ncsf; ++k) {
-      csf[k] = std::make_unique<DevCsf>();
-      outs[k] = csf[k].get();
+      owned[k] = std::make_unique<DevCsf>();
+      csf[k] = owned[k].get();
     }
-    build_csf_set(ctx, X.ind, X.vals, X.nnz, N, X.dims, roots, ncsf, outs);
+    build_csf_set(ctx, X.ind, X.vals, X.nnz, N, X.dims, roots, ncsf, csf.data());
   }
   for (int n = 0; n < N && sharded; ++n) {
-    csf[n] = std::make_unique<DevCsf>();
+    owned[n] = std::make_unique<DevCsf>();
+    csf[n] = owned[n].get();
     // this mode's selection / compaction temporaries live in the scratch arena; the local
     // tree is built into the call arena (build_csf nests its own scratch scope above ours)
     Arena* const call_arena = current_arena();

@@ -2,6 +2,8 @@
 #pragma once
 #include "ctx.hpp"
 
+struct splatt_csf;
+
 namespace sb {
 
 // COO on the device (borrowed pointers; see abi.cu for the host->device upload).
@@ -24,9 +26,11 @@ struct AlsOut {
 // Algorithm 1 on a device COO (validated here).  init: NULL or N pointers (host or
 // device, ld = R).  policy: SPLATT_CSF_ALL / ONE / TWO (ALL only when sharded).
 // Throws sb::Error.
+// prebuilt: a CSF set from splatt_csf_build (X then only supplies N, nnz and dims; no
+// validation or build) or NULL.
 void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, double tol,
                     uint64_t seed, const double* const* init, int policy, const AlsOut& out,
-                    splatt_stats* st);
+                    splatt_stats* st, const splatt_csf* prebuilt = nullptr);
 
 // C-14 partition (host).
 void host_partition(const uint64_t* w, uint64_t S, int G, uint64_t* bounds);

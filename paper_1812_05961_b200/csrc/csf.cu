@@ -391,6 +391,7 @@ void finish_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& 
 void init_tree(DevCsf& out, int N, uint64_t nnz, const uint64_t* dims, int root) {
   out.N = N;
   out.nnz = nnz;
+  out.arena = current_arena();
   csf_perm(N, dims, root, out.perm);
   for (int l = 0; l < N; ++l) {
     out.hot_ready[l] = false;
@@ -509,7 +510,7 @@ void tile_tree(splatt_ctx* ctx, DevCsf& c, int T) {
   const int N = c.N;
   const uint64_t nnz = c.nnz;
   const uint64_t rows = (c.dims[N - 1] + T - 1) / T;
-  Arena* const out_arena = current_arena();
+  Arena* const out_arena = c.arena;  // the tiles live as long as the tree
   if (out_arena && !ctx->arena_scratch) ctx->arena_scratch = new Arena();
   ArenaScope scratch(out_arena ? ctx->arena_scratch : nullptr, true);
   const int grid = grid_for(ctx, nnz);
@@ -566,6 +567,7 @@ void tile_tree(splatt_ctx* ctx, DevCsf& c, int T) {
     auto tile = std::make_unique<DevCsf>();
     tile->N = N;
     tile->nnz = n;
+    tile->arena = out_arena;
     for (int l = 0; l < N; ++l) {
       tile->perm[l] = c.perm[l];
       tile->dims[l] = c.dims[l];
@@ -592,6 +594,7 @@ void tile_tree(splatt_ctx* ctx, DevCsf& c, int T) {
 void ensure_chunk_table(splatt_ctx* ctx, DevCsf& c, int chunk) {
   if (c.tab_chunk == chunk && c.tab.p) return;
   c.nchunks = ceil_div(c.nnz, chunk);
+  ArenaScope own(c.arena, false);  // lives as long as the tree
   c.tab.alloc(c.nchunks * c.N, ctx->stream);
   PtrSet ps{};
   ps.N = c.N;

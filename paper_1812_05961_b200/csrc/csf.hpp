@@ -35,6 +35,10 @@ struct DevCsf {
   // level order holding the nonzeros whose leaf id falls in its range), run one after another.
   std::vector<std::unique_ptr<DevCsf>> tiles;
   uint64_t tile_rows = 0;  // leaf ids per tile (0 = not tiled)
+  // Allocator the tree was built from (nullptr: the stream-ordered pool).  Members built
+  // lazily (chunk table, seam rows, tiles) come from the same one, so they live as long as
+  // the tree: a call-arena tree dies with its call, a splatt_csf_build tree with its handle.
+  Arena* arena = nullptr;
 };
 
 // Split c by leaf id into T tiles of ceil(I_leaf / T) ids (tiles empty of nonzeros skipped).

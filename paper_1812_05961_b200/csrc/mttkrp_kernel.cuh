@@ -519,6 +519,7 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
   a.vals = c.vals.p;
   a.out = out;
   a.tab = c.tab.p;
+  ArenaScope own(c.arena, false);  // per-tree scratch lives as long as the tree
   if (D == 0) {
     if (c.seam.n < c.nchunks * (size_t)ld) c.seam.alloc(c.nchunks * (size_t)ld, ctx->stream);
     a.seam = c.seam.p;

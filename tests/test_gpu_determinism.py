@@ -96,3 +96,26 @@ def test_deterministic_with_leaf_tiles(sb):
         b = sb.mttkrp(csf, n, fd, rank=R).cpu().numpy()
         assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
         assert rel_fro(a, oracle.mttkrp(t.dims, t.ind, t.vals, F, n)) <= MTTKRP_TOL
+
+
+@pytest.mark.parametrize("policy", ["all", "one", "two"])
+def test_cpd_als_on_prebuilt_csf(sb, policy):
+    """splatt_cpd_als_csf: the same ALS as splatt_cpd_als on the trees of a prebuilt set,
+    repeatedly (rank sweep, seeds) without rebuilding; deterministic mode makes the ALL-policy
+    result bitwise equal to the COO entry point's."""
+    t = synth.generate((4000, 1100, 7500), 150_000, [("zipf", 1.1)] * 3, "ratings", seed=22)
+    ctx = sb.Context(0)
+    ctx.set_deterministic(True)
+    ind, vals = dev_coo(t)
+    csf = sb.csf_build(ind, vals, t.dims, ctx=ctx, policy=policy)
+    for R, seed in ((8, 1), (16, 5), (8, 1)):
+        res = sb.cpd_als_csf(csf, rank=R, max_iters=4, seed=seed, out_device=False, stats=True)
+        ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=R, max_iters=4, seed=seed)
+        als_compare(res, ref)
+        assert res["stats"]["t_build"] < 0.05  # no CSF build inside the call
+        if policy == "all":
+            coo = sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=4, seed=seed, ctx=ctx,
+                             out_device=False)
+            for n in range(3):
+                assert np.array_equal(res["factors"][n], coo["factors"][n]) or \
+                    rel_fro(res["factors"][n], coo["factors"][n]) <= 1e-12
