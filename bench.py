@@ -223,7 +223,7 @@ def config_block(cfg, G, policy="all"):
     return {"workload": cfg["name"], "dims": list(cfg["dims"]), "nnz": cfg["nnz"],
             "rank": cfg["rank"], "iters": cfg["iters"], "seed": cfg["seed"],
             "csf_policy": policy,
-            "parallelism": (f"nnz-partitioned x{G} (P2)" if G > 1 else "single GPU"),
+            "parallelism": (f"root-mode partitioned x{G} (P1/P2 per mode)" if G > 1 else "single GPU"),
             "l2": "inputs larger than L2 (COO + per-mode CSFs >> 126 MB); no explicit flush"}
 
 
@@ -245,8 +245,8 @@ def main():
                     help="CSF allocation policy (SPLATT_CSF_*)")
     ap.add_argument("--leaf-tiling", type=float, default=0.0,
                     help="ROOT MTTKRP leaf tiling above this fraction of L2 (0 = off)")
-    ap.add_argument("--partition", default="nnz", choices=["nnz", "slices"],
-                    help="multi-GPU split: equal nonzero ranges (P2) or whole slices (P1)")
+    ap.add_argument("--partition", default="auto", choices=["auto", "nnz", "slices"],
+                    help="multi-GPU split: per-mode auto, equal nonzero ranges (P2), whole slices (P1)")
     args = ap.parse_args()
 
     import synth

@@ -145,7 +145,10 @@ splatt_status splatt_comm_unique_id(void* id128);
 splatt_status splatt_ctx_set_comm(splatt_ctx* ctx, const void* id128, int nranks, int rank);
 
 /* How a sharded context splits each mode's nonzeros:
- *   SLICES (default, P1): contiguous ranges of whole root slices, the optimal cut of C-14
+ *   AUTO (default): per mode, NNZ where the best SLICES cut leaves a rank more than
+ *           max(1% of nnz/G, 2^18) nonzeros above the mean (the excess MTTKRP time then
+ *           outweighs NNZ's extra small all-reduce), else SLICES.
+ *   SLICES (P1): contiguous ranges of whole root slices, the optimal cut of C-14
  *           (splatt_partition); every rank owns the rows of its slices.  Load imbalance is
  *           bounded by the heaviest slice (power-law tensors: up to 14% of nnz in one slice).
  *   NNZ (P2, §8(f) NEXT-2): the mode's nonzeros in slice-major order (slices ascending, a
@@ -155,7 +158,7 @@ splatt_status splatt_ctx_set_comm(splatt_ctx* ctx, const void* id128, int nranks
  *           summed into it with one all-reduce of (split slices) x ld doubles per mode,
  *           before the solve.  Results differ from SLICES by rounding only.
  * Errors: BADINPUT (unknown mode).                                                       */
-enum { SPLATT_PART_SLICES = 0, SPLATT_PART_NNZ = 1 };
+enum { SPLATT_PART_SLICES = 0, SPLATT_PART_NNZ = 1, SPLATT_PART_AUTO = 2 };
 splatt_status splatt_ctx_set_partition(splatt_ctx* ctx, int32_t mode);
 
 /* In-process loopback group (testing/emulation of the sharded path on ONE device): nranks

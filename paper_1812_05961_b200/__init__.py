@@ -226,10 +226,12 @@ class Context:
         _raise(lib().splatt_ctx_set_comm(self._p, raw, world, rank), self._p)
         self.nranks, self.rank = world, rank
 
-    def set_partition(self, mode: str = "slices"):
+    def set_partition(self, mode: str = "auto"):
         """How a sharded context splits each mode: "slices" (P1, whole root slices, the
-        C-14 cut) or "nnz" (P2, equal nonzero ranges, split slices exchanged)."""
-        _raise(lib().splatt_ctx_set_partition(self._p, {"slices": 0, "nnz": 1}[mode]), self._p)
+        C-14 cut), "nnz" (P2, equal nonzero ranges, split slices exchanged) or "auto"
+        (per mode, P2 where P1's imbalance is large; the default)."""
+        _raise(lib().splatt_ctx_set_partition(self._p, {"slices": 0, "nnz": 1, "auto": 2}[mode]),
+               self._p)
 
     def set_deterministic(self, on: bool = True):
         """Bitwise-reproducible ROOT MTTKRP (fixed-order chunk-seam sums instead of atomics)."""

@@ -204,7 +204,8 @@ splatt_status splatt_ctx_set_leaf_tiling(splatt_ctx* ctx, double l2_fraction) {
 }
 
 splatt_status splatt_ctx_set_partition(splatt_ctx* ctx, int32_t mode) {
-  if (!ctx || (mode != SPLATT_PART_SLICES && mode != SPLATT_PART_NNZ)) return SPLATT_ERR_BADINPUT;
+  if (!ctx || (mode != SPLATT_PART_SLICES && mode != SPLATT_PART_NNZ && mode != SPLATT_PART_AUTO))
+    return SPLATT_ERR_BADINPUT;
   ctx->part_mode = mode;
   return SPLATT_OK;
 }

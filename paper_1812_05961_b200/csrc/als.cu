@@ -239,7 +239,8 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     csf_policy(N, X.dims, policy, &ncsf, roots, mode_csf, mode_level);
   }
   std::vector<std::vector<uint64_t>> bounds(N);
-  std::vector<NnzPart> nnzpart(N);  // P2 only
+  std::vector<NnzPart> nnzpart(N);  // P2 modes only
+  std::vector<bool> used_p2(N, false);
   size_t max_slots = 0;
   std::vector<std::unique_ptr<DevCsf>> owned(std::max(N, ncsf));  // trees built by this call
   std::vector<DevCsf*> csf(std::max(N, ncsf), nullptr);
@@ -271,7 +272,23 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     DevBuf<uint32_t> flag(X.nnz, s), pos(X.nnz, s);
     uint64_t local = 0;
     std::vector<DevBuf<uint32_t>> rk(2);
-    if (ctx->part_mode == SPLATT_PART_NNZ) {  // P2: equal leaf ranges, slices may split
+    bool use_p2 = ctx->part_mode == SPLATT_PART_NNZ;
+    if (ctx->part_mode == SPLATT_PART_AUTO) {
+      // P2 only where the best whole-slice cut leaves a rank with enough excess nonzeros to
+      // outweigh the extra small all-reduce per mode
+      std::vector<uint64_t> b1(G + 1);
+      host_partition(hc.data(), X.dims[n], G, b1.data());
+      uint64_t mx = 0;
+      for (int g = 0; g < G; ++g) {
+        uint64_t load = 0;
+        for (uint64_t i = b1[g]; i < b1[g + 1]; ++i) load += hc[i];
+        mx = std::max(mx, load);
+      }
+      const double mean = (double)X.nnz / G;
+      use_p2 = (double)mx - mean > std::max(0.01 * mean, (double)(1u << 18));
+    }
+    used_p2[n] = use_p2;
+    if (use_p2) {  // P2: equal leaf ranges, slices may split
       host_partition_nnz(hc.data(), X.dims[n], G, me, nnzpart[n]);
       const NnzPart& np = nnzpart[n];
       bounds[n] = np.rowb;
@@ -420,7 +437,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       } else {
         SB_CUDA(cudaMemsetAsync(M.p, 0, X.dims[n] * ld * sizeof(double), s));
       }
-      if (sharded && ctx->part_mode == SPLATT_PART_NNZ && !nnzpart[n].slots.empty()) {
+      if (sharded && used_p2[n] && !nnzpart[n].slots.empty()) {
         // P2: rows of slices split across ranks are summed into their owners' M rows
         const NnzPart& np = nnzpart[n];
         const size_t nsl = np.slots.size();

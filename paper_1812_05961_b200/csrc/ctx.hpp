@@ -40,7 +40,7 @@ struct splatt_ctx {
   size_t l2_bytes = 0;
   std::string err;
   uint64_t kernel_launches = 0;
-  int part_mode = SPLATT_PART_SLICES;  // sharded path: P1 (whole slices) or P2 (equal nnz)
+  int part_mode = SPLATT_PART_AUTO;    // sharded path: P1 / P2 per mode (SPLATT_PART_*)
   double leaf_tile_frac = 0.0;         // ROOT MTTKRP leaf tiling (0 = off)
   bool deterministic = false;          // ROOT MTTKRP seams: fixed-order sums, no atomics
   uint64_t host_syncs = 0;       // blocking stream syncs issued by the library

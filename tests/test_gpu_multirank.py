@@ -58,7 +58,7 @@ def run_ranks(sb, t, G, R, iters, seed, tol=0.0, partition="slices"):
     return results
 
 
-@pytest.mark.parametrize("partition", ["slices", "nnz"])
+@pytest.mark.parametrize("partition", ["slices", "nnz", "auto"])
 @pytest.mark.parametrize("G", [2, 3, 4, 8])
 def test_sharded_als_matches_single_rank_and_oracle(sb, G, partition):
     t = synth.generate((4000, 1100, 7500), 150_000, [("zipf", 1.1)] * 3, "ratings", seed=22)
@@ -147,3 +147,25 @@ def test_nccl_single_rank_sharded_path(sb):
     for n in range(3):
         assert rel_fro(res["factors"][n], ref["factors"][n]) <= ALS_TOL
     assert abs(res["fit"] - ref["fit"]) <= ALS_TOL * abs(ref["fit"])
+
+
+def test_auto_partition_picks_p2_for_heavy_mode(sb):
+    """AUTO: a mode whose heaviest slice holds 40% of 4M nonzeros gets the equal-nnz split
+    (shares within one nonzero), the others stay whole-slice; the model still matches."""
+    rng = np.random.default_rng(41)
+    base = synth.generate((20_000, 3_000, 9_000), 2_400_000, [("uniform",)] * 3, "ratings", seed=41)
+    heavy = np.stack([np.full(1_600_000, 123, np.uint32),
+                      rng.integers(0, 3_000, 1_600_000).astype(np.uint32),
+                      rng.integers(0, 9_000, 1_600_000).astype(np.uint32)], 1)
+    coords = np.unique(np.concatenate([np.stack(base.ind, 1), heavy]), axis=0)
+    coords = coords[rng.permutation(len(coords))]
+    t = synth.SparseTensor((20_000, 3_000, 9_000), [coords[:, m].copy() for m in range(3)],
+                           rng.integers(1, 6, len(coords)).astype(np.float64))
+    multi = run_ranks(sb, t, 4, 8, 2, seed=6, partition="auto")
+    ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=8, max_iters=2, seed=6)
+    for r in range(4):
+        for n in range(3):
+            assert rel_fro(multi[r]["factors"][n], ref["factors"][n]) <= ALS_TOL
+        assert abs(multi[r]["fit"] - ref["fit"]) <= ALS_TOL * abs(ref["fit"])
+    loc0 = [multi[r]["stats"]["csf_nodes"][0][2] for r in range(4)]
+    assert sum(loc0) == t.nnz and max(loc0) - min(loc0) <= 1  # mode 0: P2
