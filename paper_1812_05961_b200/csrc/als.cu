@@ -454,8 +454,9 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
                                     cudaMemcpyDeviceToDevice, s));
         tm.end();
       }
-      SB_CUDA(cudaStreamWaitEvent(s, ctx->ev_aux, 0));  // V^-1 of mode n is ready
-      tm.gap();
+      // V^-1 of mode n is ready (no stream work: the solve's span starts where the MTTKRP's
+      // ended, and includes any wait for the side stream)
+      SB_CUDA(cudaStreamWaitEvent(s, ctx->ev_aux, 0));
       // M V^-1 + statistics; single rank: the reduction kernel also forms lambda, G_n, sig
       // (line 6); sharded: the statistics are all-reduced first.
       const LambdaOut lo_fused{it == 1, lambda.p, Gall.p + n * RR, inner.p, sig.p + (size_t)n * R,
