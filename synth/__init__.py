@@ -172,11 +172,82 @@ def generate(dims, nnz, dists, values="u01", seed=0) -> SparseTensor:
     return SparseTensor(dims, ind, np.ascontiguousarray(vals, dtype=np.float64), meta)
 
 
-def generate_config(name: str, seed=None, nnz=None, dims=None) -> SparseTensor:
-    """A BASELINE.json config (optionally re-seeded or shrunk for parity tests)."""
+def _cache_dir():
+    import os
+    return os.environ.get("SPLATT_SYNTH_CACHE",
+                          os.path.join(os.path.expanduser("~"), ".cache", "splatt_b200_synth"))
+
+
+def _cache_paths(name, spec):
+    import hashlib
+    import json
+    import os
+    key = hashlib.sha256(json.dumps(spec, sort_keys=True).encode()).hexdigest()[:16]
+    base = os.path.join(_cache_dir(), f"{name}-{key}")
+    return base + ".bin", base + ".json"
+
+
+def _cache_load(name, spec):
+    """The cached tensor if its manifest matches `spec` and the payload's SHA-256 checks."""
+    import hashlib
+    import json
+    import os
+    binp, manp = _cache_paths(name, spec)
+    try:
+        with open(manp) as f:
+            man = json.load(f)
+        if man.get("spec") != spec or os.path.getsize(binp) != man["bytes"]:
+            return None
+        raw = np.fromfile(binp, dtype=np.uint8)
+        if hashlib.sha256(raw.tobytes()).hexdigest() != man["sha256"]:
+            return None
+    except (OSError, ValueError, KeyError):
+        return None
+    nnz, N = spec["nnz"], len(spec["dims"])
+    ind = [np.frombuffer(raw, dtype="<u4", count=nnz, offset=4 * nnz * m).copy() for m in range(N)]
+    vals = np.frombuffer(raw, dtype="<f8", count=nnz, offset=4 * nnz * N).copy()
+    return SparseTensor(tuple(spec["dims"]), ind, vals, dict(man.get("meta", {})))
+
+
+def _cache_store(name, spec, t):
+    """Little-endian uint32 indices then float64 values, plus a JSON manifest with the
+    recipe and the payload's SHA-256 (SURVEY.md §8(d) generator step 6).  Best effort."""
+    import hashlib
+    import json
+    import os
+    binp, manp = _cache_paths(name, spec)
+    try:
+        os.makedirs(os.path.dirname(binp), exist_ok=True)
+        payload = b"".join([np.ascontiguousarray(a, dtype="<u4").tobytes() for a in t.ind] +
+                           [np.ascontiguousarray(t.vals, dtype="<f8").tobytes()])
+        tmp = binp + f".tmp{os.getpid()}"
+        with open(tmp, "wb") as f:
+            f.write(payload)
+        os.replace(tmp, binp)
+        man = dict(spec=spec, bytes=len(payload), sha256=hashlib.sha256(payload).hexdigest(),
+                   meta={k: v for k, v in t.meta.items() if isinstance(v, (int, float, str, list))})
+        with open(manp + f".tmp{os.getpid()}", "w") as f:
+            json.dump(man, f)
+        os.replace(manp + f".tmp{os.getpid()}", manp)
+    except OSError:
+        pass
+
+
+def generate_config(name: str, seed=None, nnz=None, dims=None, cache=True) -> SparseTensor:
+    """A BASELINE.json config (optionally re-seeded or shrunk for parity tests).  Large
+    tensors are cached on disk (manifest + SHA-256; SPLATT_SYNTH_CACHE, default
+    ~/.cache/splatt_b200_synth) and re-generated whenever the cache does not verify: the
+    result is the same either way."""
     c = CONFIGS[name]
-    t = generate(dims or c["dims"], nnz or c["nnz"], c["dists"], c["values"],
-                 c["seed"] if seed is None else seed)
+    spec = dict(dims=list(dims or c["dims"]), nnz=int(nnz or c["nnz"]),
+                dists=[list(d) for d in c["dists"]], values=c["values"],
+                seed=int(c["seed"] if seed is None else seed))
+    use_cache = cache and spec["nnz"] >= 10_000_000
+    t = _cache_load(name, spec) if use_cache else None
+    if t is None:
+        t = generate(spec["dims"], spec["nnz"], c["dists"], c["values"], spec["seed"])
+        if use_cache:
+            _cache_store(name, spec, t)
     t.meta.update(config=name, rank=c["rank"], iters=c["iters"])
     return t
 
