@@ -6,6 +6,12 @@
 
 namespace sb {
 
+// Privatised hot output rows per lane group in the INTERNAL / LEAF MTTKRP.
+#ifndef SB_HOT_ROWS
+#define SB_HOT_ROWS 8
+#endif
+constexpr int kHotRows = SB_HOT_ROWS;
+
 // One CSF tree.  Level l < N-1: ids[l] (nodes[l]) and ptr[l] (nodes[l]+1, offsets into
 // level l+1); leaf level N-1: ids[N-1] (nnz) and vals (nnz).  perm[l] = mode at level l.
 struct DevCsf {
@@ -26,9 +32,9 @@ struct DevCsf {
   DevBuf<double> tail;  // deterministic mode: the open slice's row at each chunk end
   DevBuf<uint32_t> seamrows;  // deterministic mode: head / tail output rows per chunk
   uint64_t dims[SPLATT_MAX_NMODES] = {0};  // length of the mode at each level
-  // Non-root MTTKRP: the 8 most frequent ids of each level (~0u = unused), computed on
+  // Non-root MTTKRP: the kHotRows (8) most frequent ids of each level (~0u = unused), computed on
   // first use of that level as an output level.
-  uint32_t hot[SPLATT_MAX_NMODES][8];
+  uint32_t hot[SPLATT_MAX_NMODES][kHotRows];
   bool hot_ready[SPLATT_MAX_NMODES] = {false};
   // Leaf-mode tiling for the ROOT MTTKRP: when the leaf factor does
   // not fit in L2, the same tree split by leaf-id range into tiles (each a tree with the same

@@ -65,7 +65,7 @@ __global__ void id_histogram_kernel(const uint32_t* __restrict__ ids, uint64_t n
     atomicAdd(&cnt[ids[j]], 1u);
 }
 
-// The 8 most frequent ids of CSF level `level` (ties -> lower id), once per tree.
+// The kHotRows most frequent ids of CSF level `level` (ties -> lower id), once per tree.
 void ensure_hot(splatt_ctx* ctx, DevCsf& c, int level) {
   if (c.hot_ready[level]) return;
   const uint64_t I = c.dims[level], n = c.nodes[level];
@@ -80,11 +80,11 @@ void ensure_hot(splatt_ctx* ctx, DevCsf& c, int level) {
   host_sync(ctx);
   std::vector<uint32_t> idx(I);
   for (uint64_t i = 0; i < I; ++i) idx[i] = (uint32_t)i;
-  const size_t k = std::min<size_t>(8, I);
+  const size_t k = std::min<size_t>(kHotRows, I);
   std::partial_sort(idx.begin(), idx.begin() + k, idx.end(), [&](uint32_t a, uint32_t b) {
     return h[a] != h[b] ? h[a] > h[b] : a < b;
   });
-  for (int j = 0; j < 8; ++j)
+  for (int j = 0; j < kHotRows; ++j)
     c.hot[level][j] = ((size_t)j < k && h[idx[j]] > 1) ? idx[j] : ~0u;
   c.hot_ready[level] = true;
 }

@@ -58,7 +58,7 @@ struct Args {
   uint32_t nnz, nchunks, chunk;
   uint32_t ld;
   int R;
-  uint32_t hot[8];            // D > 0: the output level's most frequent ids (~0u = none)
+  uint32_t hot[kHotRows];     // D > 0: the output level's most frequent ids (~0u = none)
   int accumulate;             // D = 0: owned rows are added to `out` (later leaf tiles)
   // D = 0, deterministic mode (splatt_ctx_set_deterministic): the chunk-seam rows are not
   // added with atomics but left per chunk (head row in `seam`, tail row in `tail`, their
@@ -186,7 +186,7 @@ __host__ __device__ constexpr int group_smem_words() {
 // kHot most frequent output ids (chosen at CSF build time) and adds them to global memory
 // once, when the group finishes.
 constexpr int kRedBufs = 4;  // staging rows per lane group (ring)
-constexpr int kHot = 8;      // privatised hot output rows per lane group
+constexpr int kHot = kHotRows;  // privatised hot output rows per lane group
 template <int D>
 __host__ __device__ constexpr int group_red_doubles(int ld) {
   // + 2 doubles: the groups of a warp start in different 16-byte bank windows (as the tables)
@@ -563,7 +563,7 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
         &occ, mttkrp_csf_kernel<N, D, G, U, MINB>, threads, smem));
     occ = std::max(occ, 1);
     blocks = std::min<uint64_t>(blocks, (uint64_t)ctx->num_sms * occ);
-    for (int h = 0; h < 8; ++h) a.hot[h] = c.hot[D][h];
+    for (int h = 0; h < kHotRows; ++h) a.hot[h] = c.hot[D][h];
   }
   mttkrp_csf_kernel<N, D, G, U, MINB>
       <<<(unsigned)std::max<uint64_t>(1, blocks), threads, smem, ctx->stream>>>(a);
