@@ -61,13 +61,16 @@ enum { SPLATT_MAX_NMODES = 8, SPLATT_MAX_RANK = 128 };
  *   ONE: one CSF rooted at the shortest mode (ties -> lowest id), the other modes below
  *        it by ascending length; the mode at level l > 0 runs the INTERNAL (l < N-1) or
  *        LEAF (l = N-1) kernel, whose output rows are shared between parents and are
- *        accumulated with fp64 atomics (the GPU's replacement of the paper's mutex pool).
+ *        accumulated with asynchronous bulk fp64 reductions at L2 (the hottest rows
+ *        privatised per lane group first) — the GPU's replacement of the paper's mutex
+ *        pool.
  *   TWO: ONE's CSF plus one rooted at the longest mode (the last in ascending-length
  *        order); both roots run ROOT kernels, every other mode its level in the first.  */
 enum { SPLATT_CSF_ALL = 0, SPLATT_CSF_ONE = 1, SPLATT_CSF_TWO = 2 };
 
 typedef struct splatt_ctx splatt_ctx;   /* device, stream, allocator pool, optional comm */
-typedef struct splatt_csf splatt_csf;   /* device-resident CSF set, immutable after build */
+typedef struct splatt_csf splatt_csf;   /* device-resident CSF set (trees immutable; MTTKRP
+                                           scratch built lazily, see splatt_mttkrp)      */
 typedef struct splatt_loopback splatt_loopback; /* in-process group of logical ranks     */
 
 /* Sparse tensor in coordinate form (SoA).  nmodes in [3, 8]; nnz >= 1;
