@@ -408,13 +408,27 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   // refresh, ev_aux (aux -> main) before each solve.  Buffers shared by the two streams
   // (Vinv, Gall, lambda, inner, status) are written by one side only after the other
   // side's reads are ordered before it by these two events.
-  const bool fit_on_aux = !(tol > 0.0);  // with tol > 0 the host reads every fit
+  // Convergence (C-11) without a host round trip per iteration: with tol > 0 the fit kernel
+  // marks the iteration at which |fit_it - fit_{it-1}| < tol in a device word, every loop
+  // kernel returns at once when it is set (splatt_ctx::d_conv), and the host reads it only
+  // every kCheck iterations — the state is the converged one, the extra iterations are
+  // no-ops.
+  constexpr int kCheck = 8;
+  const bool check = tol > 0.0;
+  DevBuf<int> conv(1, s);
+  SB_CUDA(cudaMemsetAsync(conv.p, 0, sizeof(int), s));
+  struct ConvScope {
+    splatt_ctx* c;
+    ~ConvScope() { c->d_conv = nullptr; }
+  } conv_scope{ctx};
+  ctx->d_conv = check ? conv.p : nullptr;
   auto launch_aux = [&](int next, bool with_fit, int it) {
     SB_CUDA(cudaEventRecord(ctx->ev_ready, s));
     SB_CUDA(cudaStreamWaitEvent(aux, ctx->ev_ready, 0));
     if (with_fit) {
       tma.begin(kFit);
-      fit(ctx, Gall.p, N, R, lambda.p, inner.p, normx.p, fit_hist.p + (it - 1), aux);  // line 13
+      fit(ctx, Gall.p, N, R, lambda.p, inner.p, normx.p, fit_hist.p + (it - 1), it, tol,
+          check ? conv.p : nullptr, aux);  // line 13
       tma.end();
     }
     if (next >= 0) {
@@ -478,23 +492,15 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       }
       const bool last = (n == N - 1);
       const bool more = !(last && it == max_iters);
-      launch_aux(more ? (n + 1) % N : -1, last && fit_on_aux, it);
+      launch_aux(more ? (n + 1) % N : -1, last, it);
     }
     it_done = it;
-    if (!fit_on_aux) {
-      SB_CUDA(cudaStreamWaitEvent(s, ctx->ev_aux, 0));
-      tm.gap();
-      tm.begin(kFit);
-      fit(ctx, Gall.p, N, R, lambda.p, inner.p, normx.p, fit_hist.p + (it - 1));   // line 13
-      tm.end();
-      if (it >= 2) {
-        double two[2];
-        SB_CUDA(cudaMemcpyAsync(two, fit_hist.p + (it - 2), 2 * sizeof(double),
-                                cudaMemcpyDeviceToHost, s));
-        host_sync(ctx);
-        if (std::fabs(two[1] - two[0]) < tol) break;                        // C-11
-        tm.gap();
-      }
+    if (check && it % kCheck == 0 && it < max_iters) {
+      int h_conv = 0;
+      SB_CUDA(cudaStreamWaitEvent(s, ctx->ev_aux, 0));  // after this iteration's fit
+      SB_CUDA(cudaMemcpyAsync(&h_conv, conv.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      host_sync(ctx);
+      if (h_conv) break;                                                     // C-11
     }
   }
   SB_CUDA(cudaStreamWaitEvent(s, ctx->ev_aux, 0));  // the aux stream's last work
@@ -510,8 +516,9 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
                               R * sizeof(double), X.dims[n], cudaMemcpyDefault, s));
   }
   SB_CUDA(cudaMemcpyAsync(out.lambda, lambda.p, R * sizeof(double), cudaMemcpyDefault, s));
-  int h_status = 0;
+  int h_status = 0, h_conv = 0;
   SB_CUDA(cudaMemcpyAsync(&h_status, status.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SB_CUDA(cudaMemcpyAsync(&h_conv, conv.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   SB_CUDA(cudaMemcpyAsync(h_hist.data(), fit_hist.p, max_iters * sizeof(double),
                           cudaMemcpyDeviceToHost, s));
   if (st) SB_CUDA(cudaEventRecord(call_b, s));
@@ -529,6 +536,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     cudaEventDestroy(call_b);
   }
   if (h_status) fail(SPLATT_ERR_SINGULAR, "Gram Hadamard product is singular (after ridge)");
+  if (h_conv) it_done = h_conv;  // later enqueued iterations were no-ops
   *out.fit = h_hist[it_done - 1];
   *out.iters = it_done;
   if (out.fit_history)

@@ -43,6 +43,10 @@ struct splatt_ctx {
   int part_mode = SPLATT_PART_AUTO;    // sharded path: P1 / P2 per mode (SPLATT_PART_*)
   double leaf_tile_frac = 0.0;         // ROOT MTTKRP leaf tiling (0 = off)
   bool deterministic = false;          // ROOT MTTKRP seams: fixed-order sums, no atomics
+  // During an ALS call with tol > 0: device int, the iteration at which the fit stopped
+  // improving (0 = still running).  Kernels of the loop return at once when it is set, so
+  // the host enqueues iterations ahead without a sync per iteration (nullptr otherwise).
+  const int* d_conv = nullptr;
   uint64_t host_syncs = 0;       // blocking stream syncs issued by the library
   double host_sync_s = 0.0;      // host seconds spent in them
   sb::Arena* arena_call = nullptr;       // per-call buffers of cpd_als (see sb::Arena)

@@ -85,8 +85,10 @@ __global__ void sum_partials_kernel(const double* __restrict__ part, int P, doub
 // over the matrix (two barriers), so the kernel is R short steps, not R^2 serial ones.
 __global__ void hadamard_inverse_kernel(const double* __restrict__ G_all, int N, int n, int R,
                                         int ld, double* __restrict__ Vinv, int* status,
-                                        const double* __restrict__ sig, double* __restrict__ tau) {
+                                        const double* __restrict__ sig, double* __restrict__ tau,
+                                        const int* conv) {
   extern __shared__ double sm[];
+  if (conv && *conv) return;
   double* A = sm;            // R x R working matrix
   double* prow = A + R * R;  // pivot row of the current step (R)
   double* pcol = prow + R;   // pivot column of the current step (R)
@@ -196,6 +198,7 @@ struct RowsArgs {
   const double* Vinv;
   const double* tau;  // R column scales of M (stored -> true MTTKRP), folded into Vinv's rows
   const int* status;
+  const int* conv;  // ALS converged: skip (splatt_ctx::d_conv)
   double* part;  // gridDim.x x stats_len(R)
   bool solve;
 };
@@ -224,7 +227,7 @@ __global__ void __launch_bounds__(BT, kMaxBP == 1 ? (BT == 128 ? 4 : 2) : 1)
   double* tiles = taus + (a.solve ? ld : 0);         // 2 x T x ldp (+ combine area)
   if (a.solve)
     for (int r = threadIdx.x; r < ld; r += blockDim.x) taus[r] = (r < R) ? a.tau[r] : 0.0;
-  const bool dead = a.status && *a.status;
+  const bool dead = (a.status && *a.status) || (a.conv && *a.conv);
   if (a.solve && !dead) {  // Vinv is ld x ld with zero pads: one contiguous async copy
     const unsigned base = (unsigned)__cvta_generic_to_shared(Ws);
     for (int e = threadIdx.x; e < ld * ld / 2; e += blockDim.x)
@@ -429,7 +432,8 @@ __device__ __forceinline__ void reduce_stats_element(const double* __restrict__ 
 }
 
 __global__ void reduce_stats_kernel(const double* __restrict__ part, int P, int R,
-                                    double* __restrict__ out) {
+                                    double* __restrict__ out, const int* conv) {
+  if (conv && *conv) return;
   const size_t SL = (size_t)R * R + R + 1;
   const size_t e = blockIdx.x * (size_t)(blockDim.x / 32) + threadIdx.x / 32;
   if (e >= SL) return;
@@ -442,9 +446,10 @@ __global__ void reduce_stats_kernel(const double* __restrict__ part, int P, int 
 __global__ void reduce_lambda_kernel(const double* __restrict__ part, int P, int R,
                                      double* __restrict__ out, int first, double* lambda,
                                      double* G, double* inner_out, double* sig,
-                                     unsigned* ticket) {
+                                     unsigned* ticket, const int* conv) {
   extern __shared__ double lam[];
   __shared__ bool last;
+  if (conv && *conv) return;  // uniform: no block takes a ticket
   const size_t SL = (size_t)R * R + R + 1;
   const size_t e = blockIdx.x * (size_t)(blockDim.x / 32) + threadIdx.x / 32;
   if (e < SL) reduce_stats_element(part, P, R, out, e);
@@ -486,8 +491,9 @@ __device__ void lambda_gram_body(const double* st, int R, int first, double* lam
 
 __global__ void lambda_gram_kernel(const double* __restrict__ st, int R, int first,
                                    double* __restrict__ lambda, double* __restrict__ G,
-                                   double* inner_out, double* sig) {
+                                   double* inner_out, double* sig, const int* conv) {
   extern __shared__ double lam[];
+  if (conv && *conv) return;
   lambda_gram_body(st, R, first, lambda, G, inner_out, sig, lam);
 }
 
@@ -512,10 +518,14 @@ __global__ void scale_kernel(double* __restrict__ A, uint64_t lo, uint64_t hi, i
   }
 }
 
+// fit_out = fit_hist + (it - 1).  With conv (tol > 0): skip once converged, and mark
+// convergence (C-11: |fit_it - fit_{it-1}| < tol, it >= 2) by writing `it` to *conv.
 __global__ void fit_kernel(const double* __restrict__ G_all, int N, int R,
                            const double* __restrict__ lambda, const double* inner,
-                           const double* normx_sq, double* fit_out) {
+                           const double* normx_sq, double* fit_out, int it, double tol,
+                           int* conv) {
   __shared__ double sh[kThreads];
+  if (conv && *conv) return;
   const int RR = R * R;
   double acc = 0.0;
   for (int e = threadIdx.x; e < RR; e += blockDim.x) {
@@ -527,7 +537,9 @@ __global__ void fit_kernel(const double* __restrict__ G_all, int N, int R,
   if (threadIdx.x == 0) {
     const double nx = normx_sq[0];
     const double res = fmax(0.0, nx + zz - 2.0 * inner[0]);
-    fit_out[0] = 1.0 - sqrt(res) / sqrt(nx);
+    const double f = 1.0 - sqrt(res) / sqrt(nx);
+    fit_out[0] = f;
+    if (conv && it >= 2 && fabs(f - fit_out[-1]) < tol) *conv = it;
   }
 }
 
@@ -583,7 +595,8 @@ void hadamard_inverse(splatt_ctx* ctx, const double* G_all, int N, int n, int R,
   }();
   (void)attr_set;
   hadamard_inverse_kernel<<<1, 1024, smem, stream ? stream : ctx->stream>>>(G_all, N, n, R, ld,
-                                                                          Vinv, status, sig, tau);
+                                                                          Vinv, status, sig, tau,
+                                                                          ctx->d_conv);
   SB_CHECK_LAUNCH(ctx);
 }
 
@@ -649,6 +662,7 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
   a.Vinv = Vinv;
   a.tau = tau;
   a.status = status;
+  a.conv = ctx->d_conv;
   a.solve = solve;
 #ifndef SB_SOLVE_MAX_PER_SM
 #define SB_SOLVE_MAX_PER_SM 3
@@ -669,9 +683,9 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
   if (fuse) {
     reduce_lambda_kernel<<<rblocks, kThreads, R * sizeof(double), s>>>(
         part.p, P, R, stats, fuse->first ? 1 : 0, fuse->lambda, fuse->G_n, fuse->inner,
-        fuse->sig, fuse->ticket);
+        fuse->sig, fuse->ticket, ctx->d_conv);
   } else {
-    reduce_stats_kernel<<<rblocks, kThreads, 0, s>>>(part.p, P, R, stats);
+    reduce_stats_kernel<<<rblocks, kThreads, 0, s>>>(part.p, P, R, stats, ctx->d_conv);
   }
   SB_CHECK_LAUNCH(ctx);
 }
@@ -679,7 +693,8 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
 void lambda_gram(splatt_ctx* ctx, const double* stats, int R, bool first, double* lambda,
                  double* G_n, double* inner_out, double* sig) {
   lambda_gram_kernel<<<1, kThreads, R * sizeof(double), ctx->stream>>>(stats, R, first ? 1 : 0,
-                                                                       lambda, G_n, inner_out, sig);
+                                                                       lambda, G_n, inner_out, sig,
+                                                                       ctx->d_conv);
   SB_CHECK_LAUNCH(ctx);
 }
 
@@ -698,9 +713,10 @@ void scale_columns(splatt_ctx* ctx, double* A, uint64_t lo, uint64_t hi, int R, 
 }
 
 void fit(splatt_ctx* ctx, const double* G_all, int N, int R, const double* lambda,
-         const double* inner, const double* normx_sq, double* fit_out, cudaStream_t stream) {
+         const double* inner, const double* normx_sq, double* fit_out, int it, double tol,
+         int* conv, cudaStream_t stream) {
   fit_kernel<<<1, kThreads, 0, stream ? stream : ctx->stream>>>(G_all, N, R, lambda, inner,
-                                                                normx_sq, fit_out);
+                                                                normx_sq, fit_out, it, tol, conv);
   SB_CHECK_LAUNCH(ctx);
 }
 

@@ -70,9 +70,11 @@ void scale_columns(splatt_ctx* ctx, double* A, uint64_t lo, uint64_t hi, int R, 
                    const double* lambda);
 
 // a10: fit = 1 - sqrt(max(0, nx + zz - 2 inner)) / sqrt(nx), zz = lambda^T (*_m G_m) lambda.
+// fit_out = the iteration's entry of the fit history (it >= 1).  conv (or NULL): device int,
+// skip when set, else set to `it` when it >= 2 and |fit - previous fit| < tol (C-11).
 void fit(splatt_ctx* ctx, const double* G_all, int N, int R, const double* lambda,
-         const double* inner, const double* normx_sq, double* fit_out,
-         cudaStream_t stream = nullptr);
+         const double* inner, const double* normx_sq, double* fit_out, int it, double tol,
+         int* conv, cudaStream_t stream = nullptr);
 
 // a11 (finalise one mode): nu_r = sqrt(G_n[r,r]); lambda_r *= nu_r (if > 0); d_r =
 // (nu_r > 0 ? nu_r : 1) / sig_r is the divisor that turns the stored rows into the output.

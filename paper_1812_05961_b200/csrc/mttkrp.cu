@@ -95,7 +95,8 @@ void ensure_hot(splatt_ctx* ctx, DevCsf& c, int level) {
 __global__ void seam_combine_kernel(const double* __restrict__ head, const double* __restrict__ tail,
                                     const uint32_t* __restrict__ headrow,
                                     const uint32_t* __restrict__ tailrow, uint64_t nchunks, int ld,
-                                    double* __restrict__ out, int accumulate) {
+                                    double* __restrict__ out, int accumulate, const int* conv) {
+  if (conv && *conv) return;
   const uint64_t c = blockIdx.x * (uint64_t)(blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (c >= nchunks) return;
@@ -157,7 +158,7 @@ void mttkrp_level(splatt_ctx* ctx, DevCsf& c, int level, const double* const* fa
       const unsigned blocks = (unsigned)ceil_div(t.nchunks, 8);
       seam_combine_kernel<<<std::max(1u, blocks), 256, 0, ctx->stream>>>(
           t.seam.p, t.tail.p, t.seamrows.p, t.seamrows.p + t.nchunks, t.nchunks, ld, out,
-          accumulate);
+          accumulate, ctx->d_conv);
       SB_CHECK_LAUNCH(ctx);
     }
   };

@@ -67,6 +67,7 @@ struct Args {
   double* tail;
   uint32_t* headrow;
   uint32_t* tailrow;
+  const int* conv;            // ALS converged (splatt_ctx::d_conv): nothing to do
 };
 
 struct d4 { double x, y, z, w; };
@@ -203,6 +204,7 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
   constexpr int MV = MetaLayout<N>::kVec;
   constexpr int KW = MetaLayout<N>::kWords;
   extern __shared__ __align__(16) uint32_t smem[];
+  if (a.conv && *a.conv) return;
   const int lane = threadIdx.x & 31;
   const int gw = lane / G;                    // group in warp
   if (gw >= Lanes<G>::kPerWarp) return;       // lanes beyond the packed groups: no work
@@ -530,6 +532,7 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
   a.ld = (uint32_t)ld;
   a.R = R;
   a.accumulate = acc;
+  a.conv = ctx->d_conv;
   if (D == 0 && ctx->deterministic) {
     if (c.tail.n < c.nchunks * (size_t)ld) c.tail.alloc(c.nchunks * (size_t)ld, ctx->stream);
     if (c.seamrows.n < 2 * c.nchunks) c.seamrows.alloc(2 * c.nchunks, ctx->stream);
