@@ -376,6 +376,7 @@ def main():
     st = [r["stats"] for r in runs]
     t_mttkrp = sum(s["t_mttkrp"] for s in st)
     alg_bytes = sum(s["mttkrp_alg_bytes"] for s in st)
+    min_bytes = sum(s["mttkrp_min_bytes"] for s in st)
     launches = sum(s["mttkrp_launches"] for s in st)
     peak, peak_src = peaks()
     achieved = alg_bytes / t_mttkrp / 1e9 if t_mttkrp > 0 else 0.0
@@ -409,6 +410,11 @@ def main():
                      "kernel": (f"mttkrp_csf_kernel<N={N}> ROOT traversal" if args.policy == "all"
                                 else f"mttkrp_csf_kernel<N={N}> ROOT/INTERNAL/LEAF ({args.policy})"), "peak_source": peak_src,
                      "alg_bytes_per_launch": alg_bytes / max(1, launches),
+                     # SURVEY.md §7 hard part 3: the compulsory-traffic view beside the
+                     # north star's every-gather-at-HBM count (tree, referenced rows and
+                     # output once per launch).
+                     "min_bytes_per_launch": min_bytes / max(1, launches),
+                     "frac_compulsory": (min_bytes / t_mttkrp / 1e9 / peak) if t_mttkrp else None,
                      "avg_launch_ms": 1e3 * t_mttkrp / max(1, launches),
                      "launches": launches},
         "gpu_launches": sum(s["kernel_launches"] for s in st),

@@ -118,6 +118,8 @@ typedef struct {
   int32_t  host_syncs;      /* host<->device synchronisations inside the call            */
   double   t_aux_inverse;   /* V^-1 (Hadamard + Gauss-Jordan) spans on the side stream,  */
   double   t_aux_fit;       /*   and fit spans: overlapped with MTTKRP, not in t_inverse  */
+  double   mttkrp_min_bytes;/* sum over launches of the compulsory bytes: tree once,      */
+                            /*   referenced factor rows once, output once */
 } splatt_stats;
 
 /* ---------------------------------------------------------------- context */

@@ -75,7 +75,8 @@ class Stats(C.Structure):
                 ("csf_nodes", (C.c_uint64 * MAX_NMODES) * MAX_NMODES),
                 ("iters", C.c_int32), ("nranks", C.c_int32), ("t_call", C.c_double),
                 ("t_host_sync", C.c_double), ("host_syncs", C.c_int32),
-                ("t_aux_inverse", C.c_double), ("t_aux_fit", C.c_double)]
+                ("t_aux_inverse", C.c_double), ("t_aux_fit", C.c_double),
+                ("mttkrp_min_bytes", C.c_double)]
 
     def to_dict(self, nmodes=None):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "csf_nodes"}

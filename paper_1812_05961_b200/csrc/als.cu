@@ -393,8 +393,22 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   tm.end();
 
   // ----------------------------------------------------------------- loop
-  double mttkrp_bytes = 0.0;
+  double mttkrp_bytes = 0.0, mttkrp_min = 0.0;
   uint64_t mttkrp_launches = 0;
+  // Rows of each mode a launch can reference, for the compulsory-traffic figure: the root
+  // node count of the mode's own (whole-tensor) tree, else min(I_m, nodes at its level).
+  auto min_bytes = [&](const DevCsf& c, int level) {
+    uint64_t distinct[SPLATT_MAX_NMODES] = {0};
+    for (int l = 0; l < N; ++l) {
+      const int m = c.perm[l];
+      uint64_t d = l == 0 ? c.nodes[0] : std::min<uint64_t>(c.dims[l], c.nodes[l]);
+      if (!sharded)
+        for (int k = 0; k < ncsf; ++k)
+          if (csf[k]->perm[0] == m) d = std::min<uint64_t>(d, csf[k]->nodes[0]);
+      distinct[m] = d;
+    }
+    return mttkrp_min_bytes(c, R, level, distinct);
+  };
   std::vector<double> h_hist(max_iters, 0.0);
   int it_done = 0;
   cudaEvent_t loop_a = nullptr, loop_b = nullptr;
@@ -447,6 +461,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       if (cn.nnz) {
         mttkrp_level(ctx, cn, mode_level[n], fac, M.p, X.dims[n], ld, R, &tm, kMttkrp);  // 5/8/11
         mttkrp_bytes += mttkrp_alg_bytes(cn, R, mode_level[n]);
+        mttkrp_min += min_bytes(cn, mode_level[n]);
         ++mttkrp_launches;
       } else {
         SB_CUDA(cudaMemsetAsync(M.p, 0, X.dims[n] * ld * sizeof(double), s));
@@ -557,6 +572,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     st->t_comm = t[kComm];
     st->t_loop = loop_ms * 1e-3;
     st->mttkrp_alg_bytes = mttkrp_bytes;
+    st->mttkrp_min_bytes = mttkrp_min;
     st->mttkrp_launches = mttkrp_launches;
     st->kernel_launches = ctx->kernel_launches - launches0;
     for (int k = 0; k < (sharded ? N : ncsf); ++k)

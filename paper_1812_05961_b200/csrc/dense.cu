@@ -408,6 +408,203 @@ __global__ void __launch_bounds__(BT, kMaxBP == 1 ? (BT == 128 ? 4 : 2) : 1)
   if (threadIdx.x == 0) out[(size_t)R * R] = tot;
 }
 
+// ------------------------------------- row solves + Gram on the fp64 tensor cores (DMMA)
+// The same contract as solve_gram_kernel for R <= 8 NT, as two small dense contractions
+// per slab of 8 rows (mma.sync m8n8k4 f64 — tcgen05 has no fp64 kind, so this is the
+// sm_100a fp64 tensor-core path):  X = M_slab (8 x ld) . Vinv (ld x 8NT)  and
+// G~ += X^T X.  Every warp works alone on its own slabs (rows lo + 8s .. +8), staged with
+// cp.async into a two-slab ring (row stride ldp = 8NT + 4 doubles: conflict-free fragment
+// loads for both products); the row solve's A operand comes from the staged M rows, its B
+// operand (Vinv, ld x 8NT, zero pads) from shared memory; the solved slab replaces the M
+// rows in shared memory (for the Gram's fragments and a coalesced write-back); column max
+// |x| and <M o tau, X> are taken from the accumulator registers.  Warps are combined in
+// fixed order at the end, so the per-CTA partial is deterministic.
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int NT>
+struct MmaShape {
+  static constexpr int RP = 8 * NT;        // padded columns
+  static constexpr int LDP = RP + 4;       // slab row stride (doubles)
+  static constexpr int NP = NT * (NT + 1) / 2;  // upper-triangular 8x8 Gram tiles
+};
+
+template <int NT, int W>
+__global__ void __launch_bounds__(W * 32, 1) solve_gram_mma_kernel(const RowsArgs a) {
+  using Sh = MmaShape<NT>;
+  constexpr int RP = Sh::RP, LDP = Sh::LDP, NP = Sh::NP;
+  constexpr int KS = RP / 4;  // k-steps upper bound (ld <= RP)
+  extern __shared__ __align__(16) double sm[];
+  const int R = a.R, ld = a.ld;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  double* Ws = sm;                                  // ld x RP (solve)
+  double* taus = Ws + (a.solve ? (size_t)ld * RP : 0);  // RP
+  double* slabs = taus + RP;                        // W x 2 x 8 x LDP
+  slabs = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(slabs) + 15) & ~uintptr_t(15));
+  double* mine = slabs + (size_t)warp * 2 * 8 * LDP;
+  const bool dead = (a.status && *a.status) || (a.conv && *a.conv);
+  // columns ld..LDP-1 of the warp's slab ring stay zero (cp.async fills columns < ld)
+  for (int e = lane; e < 2 * 8 * (LDP - ld); e += 32)
+    mine[(e / (LDP - ld)) * LDP + ld + e % (LDP - ld)] = 0.0;
+  __syncwarp();
+  const uint64_t nslabs = (a.hi - a.lo + 7) / 8;
+  const uint64_t stride = (uint64_t)gridDim.x * W;
+  const double* src = a.solve ? a.M : a.A;
+  const int half = ld / 2;
+  auto load_slab = [&](uint64_t sI, double* buf) {
+    if (sI < nslabs && !dead) {
+      const uint64_t row0 = a.lo + sI * 8;
+      for (int e = lane; e < 8 * half; e += 32) {
+        const int r = e / half, c = 2 * (e % half);
+        const bool in = row0 + r < a.hi;
+        const double* gp = src + (in ? (row0 + r) * ld + c : 0);
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(buf + r * LDP + c);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(gp),
+                     "r"(in ? 16 : 0));
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  uint64_t sI = (uint64_t)blockIdx.x * W + warp;
+  load_slab(sI, mine);  // in flight while Vinv is staged
+  if (a.solve) {
+    for (int e = threadIdx.x; e < ld * RP; e += blockDim.x) {
+      const int k = e / RP, n = e % RP;
+      Ws[e] = (n < ld) ? a.Vinv[(size_t)k * ld + n] : 0.0;
+    }
+    for (int c = threadIdx.x; c < RP; c += blockDim.x) taus[c] = (c < R) ? a.tau[c] : 0.0;
+  }
+  __syncthreads();
+
+  double gacc[NP][2];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) gacc[p][0] = gacc[p][1] = 0.0;
+  double cm[NT][2];
+#pragma unroll
+  for (int n = 0; n < NT; ++n) cm[n][0] = cm[n][1] = 0.0;
+  double inner = 0.0;
+  const int ks = ld / 4;
+
+  int cur = 0;
+  for (; sI < nslabs && !dead; sI += stride, cur ^= 1) {
+    double* buf = mine + cur * 8 * LDP;
+    load_slab(sI + stride, mine + (cur ^ 1) * 8 * LDP);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    const uint64_t row0 = a.lo + sI * 8;
+    const int nrows = (a.hi - row0) < 8 ? (int)(a.hi - row0) : 8;
+    if (a.solve) {
+      double c[NT][2];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) c[n][0] = c[n][1] = 0.0;
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
+        if (k < ks) {
+          const int kc = 4 * k + t;
+          const double av = (kc < R) ? buf[g * LDP + kc] : 0.0;
+          const double* wrow = Ws + (size_t)kc * RP + g;
+#pragma unroll
+          for (int n = 0; n < NT; ++n) dmma(c[n][0], c[n][1], av, wrow[n * 8]);
+        }
+      }
+      // <M o tau, X> for this slab, then the solved rows replace the M rows
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        const double2 m2 = *reinterpret_cast<const double2*>(buf + g * LDP + n * 8 + 2 * t);
+        const double2 t2 = *reinterpret_cast<const double2*>(taus + n * 8 + 2 * t);
+        inner = fma(m2.x * t2.x, c[n][0], inner);
+        inner = fma(m2.y * t2.y, c[n][1], inner);
+        cm[n][0] = fmax(cm[n][0], fabs(c[n][0]));
+        cm[n][1] = fmax(cm[n][1], fabs(c[n][1]));
+      }
+      __syncwarp();
+#pragma unroll
+      for (int n = 0; n < NT; ++n)
+        *reinterpret_cast<double2*>(buf + g * LDP + n * 8 + 2 * t) = make_double2(c[n][0], c[n][1]);
+      __syncwarp();
+      double2* dst = reinterpret_cast<double2*>(a.A + row0 * ld);
+      for (int e = lane; e < nrows * half; e += 32)
+        dst[e] = *reinterpret_cast<const double2*>(buf + (e / half) * LDP + 2 * (e % half));
+    } else {
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        const double2 x2 = *reinterpret_cast<const double2*>(buf + g * LDP + n * 8 + 2 * t);
+        cm[n][0] = fmax(cm[n][0], fabs(x2.x));
+        cm[n][1] = fmax(cm[n][1], fabs(x2.y));
+      }
+    }
+    // G~ += X^T X over the slab's 8 rows (rows past hi are zero)
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      double f[NT];
+#pragma unroll
+      for (int b = 0; b < NT; ++b) f[b] = buf[(kk * 4 + t) * LDP + b * 8 + g];
+      int p = 0;
+#pragma unroll
+      for (int bi = 0; bi < NT; ++bi)
+#pragma unroll
+        for (int bj = bi; bj < NT; ++bj, ++p) dmma(gacc[p][0], gacc[p][1], f[bi], f[bj]);
+    }
+    __syncwarp();  // the buffer is refilled two slabs later
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+
+  // column max over the 8 row lanes (g), inner over the warp: fixed shuffle trees
+#pragma unroll
+  for (int n = 0; n < NT; ++n)
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int o = 4; o <= 16; o <<= 1) cm[n][i] = fmax(cm[n][i], __shfl_xor_sync(0xffffffffu, cm[n][i], o));
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) inner += __shfl_xor_sync(0xffffffffu, inner, o);
+
+  // combine: every warp parks its raw fragments (NP x 32 lanes x 2 | RP colmax | inner) in
+  // its own region of the (now dead) shared memory, then all threads sum each element over
+  // the warps in fixed order and scatter it into the CTA partial (both triangles).
+  constexpr int CL = NP * 64 + RP + 1, CLS = (CL + 1) & ~1;
+  __syncthreads();
+  double* park = sm + (size_t)warp * CLS;
+#pragma unroll
+  for (int p = 0; p < NP; ++p)
+    *reinterpret_cast<double2*>(park + p * 64 + 2 * lane) = make_double2(gacc[p][0], gacc[p][1]);
+  if (g == 0)
+#pragma unroll
+    for (int n = 0; n < NT; ++n)
+      *reinterpret_cast<double2*>(park + NP * 64 + n * 8 + 2 * t) = make_double2(cm[n][0], cm[n][1]);
+  if (lane == 0) park[NP * 64 + RP] = inner;
+  __syncthreads();
+  const size_t SL = (size_t)R * R + R + 1;
+  double* out = a.part + (size_t)blockIdx.x * SL;
+  for (int e = threadIdx.x; e < CL; e += blockDim.x) {
+    const bool is_max = e >= NP * 64 && e < NP * 64 + RP;
+    double v = sm[e];
+    for (int w = 1; w < W; ++w) {
+      const double x = sm[(size_t)w * CLS + e];
+      v = is_max ? fmax(v, x) : v + x;
+    }
+    if (e < NP * 64) {
+      int p = e >> 6, bi = 0;
+      while (p >= NT - bi) { p -= NT - bi; ++bi; }
+      const int bj = bi + p, ln = (e & 63) >> 1;
+      const int r = bi * 8 + (ln >> 2), c2 = bj * 8 + 2 * (ln & 3) + (e & 1);
+      if (r < R && c2 < R) {
+        out[(size_t)r * R + c2] = v;
+        if (bi != bj) out[(size_t)c2 * R + r] = v;
+      }
+    } else if (is_max) {
+      const int c2 = e - NP * 64;
+      if (c2 < R) out[(size_t)R * R + 1 + c2] = v;
+    } else {
+      out[(size_t)R * R] = v;
+    }
+  }
+}
+
 // stats[e] = fixed-order reduction over P partials: one warp per element, lane l sums
 // partials l, l+32, ... then a fixed shuffle tree (sum; max for the colmax entries).
 __device__ void lambda_gram_body(const double* st, int R, int first, double* lambda, double* G,
@@ -626,6 +823,58 @@ void launch_rows_g(int G, const RowsArgs& a, int P, size_t smem, cudaStream_t s)
   }
 }
 
+#ifndef SB_MMA_W
+#define SB_MMA_W 8
+#endif
+constexpr int mma_warps(int NT) { return NT <= 5 ? SB_MMA_W : 8; }
+
+template <int NT>
+void launch_rows_mma_t(const RowsArgs& a, int P, size_t smem, cudaStream_t s) {
+  constexpr int W = mma_warps(NT);
+  static const bool attr = [] {
+    SB_CUDA(cudaFuncSetAttribute(solve_gram_mma_kernel<NT, W>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    return true;
+  }();
+  (void)attr;
+  solve_gram_mma_kernel<NT, W><<<P, W * 32, smem, s>>>(a);
+}
+
+void launch_rows_mma(int NT, const RowsArgs& a, int P, size_t smem, cudaStream_t s) {
+  switch (NT) {
+    case 1: return launch_rows_mma_t<1>(a, P, smem, s);
+    case 2: return launch_rows_mma_t<2>(a, P, smem, s);
+    case 3: return launch_rows_mma_t<3>(a, P, smem, s);
+    case 4: return launch_rows_mma_t<4>(a, P, smem, s);
+    case 5: return launch_rows_mma_t<5>(a, P, smem, s);
+    case 6: return launch_rows_mma_t<6>(a, P, smem, s);
+    case 7: return launch_rows_mma_t<7>(a, P, smem, s);
+    default: return launch_rows_mma_t<8>(a, P, smem, s);
+  }
+}
+
+// Fixed-order reduction of the P per-CTA partials (with the lambda / G_n step fused when
+// `fuse` is given).
+void reduce_rows_stats(splatt_ctx* ctx, const double* part, int P, int R, double* stats,
+                       const LambdaOut* fuse) {
+  const size_t SL = stats_len(R);
+  cudaStream_t s = ctx->stream;
+  const unsigned rblocks = (unsigned)ceil_div(SL, kThreads / 32);
+  if (fuse) {
+    reduce_lambda_kernel<<<rblocks, kThreads, R * sizeof(double), s>>>(
+        part, P, R, stats, fuse->first ? 1 : 0, fuse->lambda, fuse->G_n, fuse->inner,
+        fuse->sig, fuse->ticket, ctx->d_conv);
+  } else {
+    reduce_stats_kernel<<<rblocks, kThreads, 0, s>>>(part, P, R, stats, ctx->d_conv);
+  }
+  SB_CHECK_LAUNCH(ctx);
+}
+
+bool getenv_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && *v && *v != '0';
+}
+
 }  // namespace
 
 void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, uint64_t hi,
@@ -672,6 +921,29 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
   const int per_sm =
       std::max<int>(1, std::min<int>(max_res, (int)((228 * 1024) / (smem + 2048))));
   const int P = (int)std::min<uint64_t>(a.ntiles, (uint64_t)ctx->num_sms * per_sm);
+#ifndef SB_SOLVE_MMA
+#define SB_SOLVE_MMA 1
+#endif
+  const int NT = (R + 7) / 8;
+  if (SB_SOLVE_MMA && NT <= 8 && !getenv_flag("SPLATT_SOLVE_SIMT")) {
+    // fp64 tensor-core path (solve_gram_mma_kernel): one CTA per SM
+    const int W = mma_warps(NT);
+    const int RP = 8 * NT, LDP = RP + 4;
+    const size_t loop_d = (size_t)(solve ? ld : 0) * RP + RP + 2 + (size_t)W * 2 * 8 * LDP;
+    const size_t park_d = (size_t)W * (NT * (NT + 1) / 2 * 64 + RP + 2);
+    const size_t msmem = std::max(loop_d, park_d) * sizeof(double);
+    const uint64_t nslabs = ceil_div(hi - lo, 8);
+    a.ntiles = nslabs;
+    const int Pm = (int)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(nslabs, W),
+                                                                 (uint64_t)ctx->num_sms));
+    ArenaScope scratch(current_arena() ? ctx->arena_scratch : nullptr, true);  // per-launch
+    DevBuf<double> part((size_t)Pm * SL, s);
+    a.part = part.p;
+    launch_rows_mma(NT, a, Pm, msmem, s);
+    SB_CHECK_LAUNCH(ctx);
+    reduce_rows_stats(ctx, part.p, Pm, R, stats, fuse);
+    return;
+  }
   ArenaScope scratch(current_arena() ? ctx->arena_scratch : nullptr, true);  // per-launch
   DevBuf<double> part((size_t)P * SL, s);
   a.part = part.p;
@@ -679,15 +951,7 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
   else if (KB == 1) launch_rows_g<1, 256>(G, a, P, smem, s);
   else launch_rows_g<3, 256>(G, a, P, smem, s);
   SB_CHECK_LAUNCH(ctx);
-  const unsigned rblocks = (unsigned)ceil_div(SL, kThreads / 32);
-  if (fuse) {
-    reduce_lambda_kernel<<<rblocks, kThreads, R * sizeof(double), s>>>(
-        part.p, P, R, stats, fuse->first ? 1 : 0, fuse->lambda, fuse->G_n, fuse->inner,
-        fuse->sig, fuse->ticket, ctx->d_conv);
-  } else {
-    reduce_stats_kernel<<<rblocks, kThreads, 0, s>>>(part.p, P, R, stats, ctx->d_conv);
-  }
-  SB_CHECK_LAUNCH(ctx);
+  reduce_rows_stats(ctx, part.p, P, R, stats, fuse);
 }
 
 void lambda_gram(splatt_ctx* ctx, const double* stats, int R, bool first, double* lambda,

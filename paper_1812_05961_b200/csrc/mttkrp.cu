@@ -56,6 +56,20 @@ double mttkrp_alg_bytes(const DevCsf& c, int R, int level) {
   return 12.0 * (double)c.nnz + 8.0 * internal + 8.0 * R * rows;
 }
 
+double mttkrp_min_bytes(const DevCsf& c, int R, int level, const uint64_t* distinct) {
+  // Compulsory traffic of one launch: the tree once (12 B per leaf, 8 B per internal node),
+  // every factor row the launch references once (distinct[m] rows of mode m: the root node
+  // count of mode m's own tree when one exists, else min(I_m, nodes at its level) — an upper
+  // bound), and the output matrix written once (I_D rows).  SURVEY.md §7 hard part 3.
+  const int N = c.N;
+  double internal = 0.0;
+  for (int l = 0; l < N - 1; ++l) internal += (double)c.nodes[l];
+  double rows = (double)c.dims[level];
+  for (int l = 0; l < N; ++l)
+    if (l != level) rows += (double)distinct[c.perm[l]];
+  return 12.0 * (double)c.nnz + 8.0 * internal + 8.0 * R * rows;
+}
+
 namespace {
 
 __global__ void id_histogram_kernel(const uint32_t* __restrict__ ids, uint64_t n,

@@ -28,6 +28,9 @@ inline void mttkrp_root(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_
 // Algorithmic bytes of one MTTKRP over `c` at rank R for output level `level`
 // (SURVEY.md §8(d) B_alg for level 0; DESIGN.md §4.2 for the others).
 double mttkrp_alg_bytes(const DevCsf& c, int R, int level = 0);
+// Compulsory bytes of one launch (tree once, referenced factor rows once, output once);
+// distinct[m] = rows of mode m the tensor references (or an upper bound).
+double mttkrp_min_bytes(const DevCsf& c, int R, int level, const uint64_t* distinct);
 
 int mttkrp_chunk_leaves(int N, int ld);
 

@@ -227,6 +227,25 @@ def test_cpd_als_one_step_from_oracle_state(sb, ctx):
         A = [f * 1.0 for f in ref["factors"]]
 
 
+@pytest.mark.parametrize("path", ["dmma", "simt"])
+@pytest.mark.parametrize("R", [1, 5, 8, 13, 24, 35, 40, 57, 64, 65, 96])
+def test_row_solve_paths_one_step(sb, ctx, monkeypatch, R, path):
+    """Line 5's row solve + Gram/colmax/inner statistics on both kernels: the fp64
+    tensor-core one (R <= 64: every 8-column tile count 1..8, ragged last tiles) and the SIMT
+    one (forced with SPLATT_SOLVE_SIMT, and the only one beyond R = 64); one ALS step from
+    the oracle's state, twice, at the one-step tolerance."""
+    if path == "simt":
+        monkeypatch.setenv("SPLATT_SOLVE_SIMT", "1")
+    t = tensors()[2]
+    A = oracle.init_factors(t.dims, R, 11)
+    ind, vals = dev_coo(t)
+    for _ in range(2):
+        ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=R, max_iters=1, init=A)
+        res = sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=1, init=A, ctx=ctx)
+        als_compare(res, ref, tol=1e-9)
+        A = [f * 1.0 for f in ref["factors"]]
+
+
 def test_cpd_als_rank1_planted_and_host_io(sb, ctx):
     rng = np.random.default_rng(4)
     F = [rng.random((d, 1)) + 0.1 for d in (9, 7, 8)]

@@ -185,3 +185,28 @@ def test_policy_errors(sb, ctx):
     with pytest.raises(sb.BadInputError):
         sb.mttkrp(csf, 0, F, rank=2, which=1)  # ONE has a single tree
     ctx.sync()
+
+
+def test_traffic_counters_policy_all(sb, ctx):
+    """The bench's roofline inputs: per launch under ALL, B_alg (12 B per
+    leaf, 8 B per internal node, 8R B per gathered non-root row) and the compulsory bytes
+    (tree once + each referenced factor row once + output once), recomputed here from numpy
+    distinct counts and the reported node counts."""
+    t = tensors()[1]
+    R, iters = 35, 2
+    ind, vals = dev_coo(t)
+    res = sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=iters, seed=1, ctx=ctx, stats=True)
+    s, N = res["stats"], t.nmodes
+    distinct = [np.unique(t.ind[m]).size for m in range(N)]
+    alg = mn = 0.0
+    for n in range(N):
+        nodes = s["csf_nodes"][n]
+        assert nodes[0] == distinct[n] and nodes[N - 1] == t.nnz
+        internal = sum(nodes[:N - 1])
+        alg += 12 * t.nnz + 8 * internal + 8 * R * sum(nodes[1:])
+        mn += 12 * t.nnz + 8 * internal + 8 * R * (t.dims[n] + sum(
+            distinct[m] for m in range(N) if m != n))
+    assert s["mttkrp_launches"] == iters * N
+    assert s["mttkrp_alg_bytes"] == pytest.approx(iters * alg, rel=1e-12)
+    assert s["mttkrp_min_bytes"] == pytest.approx(iters * mn, rel=1e-12)
+    assert s["mttkrp_min_bytes"] < s["mttkrp_alg_bytes"]
