@@ -49,6 +49,23 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
+def gather_view(st, N, R, t_mttkrp, policy):
+    """Rows gathered by the ROOT MTTKRPs (every non-root CSF node: one factor row each) per
+    second, against the measured row-gather ceiling (profiles/gather_peak.json)."""
+    if policy != "all" or not t_mttkrp:
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "gather_peak.json")) as f:
+            gp = json.load(f)
+    except Exception:
+        return None
+    rows = sum(s["iters"] * sum(sum(s["csf_nodes"][n][1:N]) for n in range(N)) for s in st)
+    rate = rows / t_mttkrp
+    return {"rows_per_s": rate, "peak_rows_per_s": gp["rows_per_s"],
+            "frac": rate / gp["rows_per_s"], "row_bytes": 8 * ((R + 3) // 4 * 4),
+            "peak_source": "profiles/gather_peak.json (measured gather microbenchmark)"}
+
+
 class NvmlClockSampler:
     """NVML sampling (in-process thread) during the timed region: SM clock, max SM clock
     and the clock-event (throttle) reasons, the fields of the recipe's clocks line."""
@@ -415,6 +432,9 @@ def main():
                      # output once per launch).
                      "min_bytes_per_launch": min_bytes / max(1, launches),
                      "frac_compulsory": (min_bytes / t_mttkrp / 1e9 / peak) if t_mttkrp else None,
+                     # the bound that actually binds: the L1TEX row-gather rate (measured
+                     # ceiling of the gather primitive, profiles/gather_peak.json)
+                     "gather": gather_view(st, N, R, t_mttkrp, args.policy),
                      "avg_launch_ms": 1e3 * t_mttkrp / max(1, launches),
                      "launches": launches},
         "gpu_launches": sum(s["kernel_launches"] for s in st),

@@ -454,12 +454,41 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     SB_CUDA(cudaEventRecord(ctx->ev_aux, aux));
   };
   launch_aux(0, false, 0);
+  // ROOT gather cache policy per tree: iteration 1 runs L1::no_allocate,
+  // iteration 2 L1-allocating gathers, timed with events; one host sync after iteration 2
+  // picks the faster for the rest (and for later calls on the same trees).  Results do not
+  // depend on the choice.
+  struct TuneEvents {
+    cudaEvent_t e[SPLATT_MAX_NMODES][4] = {};
+    ~TuneEvents() {
+      for (auto& m : e)
+        for (auto& x : m)
+          if (x) cudaEventDestroy(x);
+    }
+  } tev_own;
+  auto& tev = tev_own.e;
+  bool tune[SPLATT_MAX_NMODES] = {false};
+  bool tuning = false;
+  if (max_iters >= 4 && !getenv("SPLATT_L1_ALLOC")) {
+    for (int n = 0; n < N; ++n) {
+      const DevCsf& cn = *csf[mode_csf[n]];
+      tune[n] = mode_level[n] == 0 && cn.l1a < 0 && cn.nnz >= (1u << 20);
+      if (tune[n]) {
+        tuning = true;
+        for (int e = 0; e < 4; ++e) SB_CUDA(cudaEventCreate(&tev[n][e]));
+      }
+    }
+  }
   for (int it = 1; it <= max_iters; ++it) {
     for (int n = 0; n < N; ++n) {
       const uint64_t lo = bounds[n][me], hi = bounds[n][me + 1];
       DevCsf& cn = *csf[mode_csf[n]];
       if (cn.nnz) {
-        mttkrp_level(ctx, cn, mode_level[n], fac, M.p, X.dims[n], ld, R, &tm, kMttkrp);  // 5/8/11
+        const bool timed = tune[n] && it <= 2;
+        if (timed) SB_CUDA(cudaEventRecord(tev[n][2 * (it - 1)], s));
+        mttkrp_level(ctx, cn, mode_level[n], fac, M.p, X.dims[n], ld, R, &tm, kMttkrp,
+                     timed ? it - 1 : -1);  // 5/8/11
+        if (timed) SB_CUDA(cudaEventRecord(tev[n][2 * (it - 1) + 1], s));
         mttkrp_bytes += mttkrp_alg_bytes(cn, R, mode_level[n]);
         mttkrp_min += min_bytes(cn, mode_level[n]);
         ++mttkrp_launches;
@@ -510,6 +539,20 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       launch_aux(more ? (n + 1) % N : -1, last, it);
     }
     it_done = it;
+    if (tuning && it == 2) {
+      host_sync(ctx);
+      for (int n = 0; n < N; ++n) {
+        if (!tune[n]) continue;
+        float t0 = 0.f, t1 = 0.f;
+        SB_CUDA(cudaEventElapsedTime(&t0, tev[n][0], tev[n][1]));
+        SB_CUDA(cudaEventElapsedTime(&t1, tev[n][2], tev[n][3]));
+        csf[mode_csf[n]]->l1a = (t1 < t0) ? 1 : 0;
+        if (getenv("SPLATT_TRACE"))
+          fprintf(stderr, "[splatt] mode %d ROOT gathers: no_allocate %.3f ms, L1-allocating %.3f ms\n",
+                  n, t0, t1);
+      }
+      tuning = false;
+    }
     if (check && it % kCheck == 0 && it < max_iters) {
       int h_conv = 0;
       SB_CUDA(cudaStreamWaitEvent(s, ctx->ev_aux, 0));  // after this iteration's fit

@@ -73,7 +73,8 @@ struct BitSet { int b[SPLATT_MAX_NMODES]; };
 // coordinate of level l at sorted position j = bits of the sorted composite key.
 __global__ void decode_kernel(KeySpec ks, BitSet bs, CoordOut co, uint64_t nnz,
                               const uint64_t* __restrict__ keys, const uint32_t* __restrict__ P,
-                              const double* __restrict__ vin, double* __restrict__ vout) {
+                              const double* __restrict__ vin, double* __restrict__ vout,
+                              double2* __restrict__ kv) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
        j += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k = keys[j];
@@ -81,7 +82,9 @@ __global__ void decode_kernel(KeySpec ks, BitSet bs, CoordOut co, uint64_t nnz,
       const uint64_t m = bs.b[l] >= 64 ? ~0ull : ((1ull << bs.b[l]) - 1ull);
       co.dst[l][j] = (uint32_t)((k >> ks.shift[l]) & m);
     }
-    vout[j] = vin[P[j]];
+    const double v = vin[P[j]];
+    vout[j] = v;
+    if (kv) kv[j] = make_double2(__longlong_as_double((long long)k), v);
   }
 }
 
@@ -231,7 +234,34 @@ namespace {
 struct SortedTree {
   DevBuf<uint32_t> coord[SPLATT_MAX_NMODES];
   DevBuf<double> vals;
+  // Q-sorted (composite key, value) pairs, one 16-byte record per nonzero (one key group
+  // only): a derived tree gathers one record per nonzero through its permutation instead of
+  // N coordinates and a value (N + 1 random reads, each a DRAM burst).
+  DevBuf<double2> kv;
+  int shift[SPLATT_MAX_NMODES] = {0}, bits[SPLATT_MAX_NMODES] = {0};
 };
+
+struct KvOut {
+  uint32_t* dst[SPLATT_MAX_NMODES];  // tree levels 1..N-1
+  int shift[SPLATT_MAX_NMODES], bits[SPLATT_MAX_NMODES];
+  int N;
+};
+
+// Derived tree: level l (>= 1) coordinate and value of sorted position j from the Q-sorted
+// record kv[P[j]] (one 16-byte read).
+__global__ void gather_kv_kernel(KvOut ko, uint64_t nnz, const uint32_t* __restrict__ P,
+                                 const double2* __restrict__ kv, double* __restrict__ vout) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const double2 r = kv[P[j]];
+    const uint64_t k = (uint64_t)__double_as_longlong(r.x);
+    for (int l = 1; l < ko.N; ++l) {
+      const uint64_t m = ko.bits[l] >= 64 ? ~0ull : ((1ull << ko.bits[l]) - 1ull);
+      ko.dst[l][j] = (uint32_t)((k >> ko.shift[l]) & m);
+    }
+    vout[j] = r.y;
+  }
+}
 
 __global__ void iota_kernel(uint32_t* __restrict__ p, uint64_t n) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
@@ -253,6 +283,7 @@ __global__ void gather_levels_kernel(CoordOut co, uint64_t nnz, const uint32_t* 
 // Full sort of the COO into the order of `perm`: packed composite keys (one or more <= 64-bit
 // groups, LSD), stable radix sort of (key, position), then decode / gather into t (allocated
 // by the caller, alloc_sorted).
+// If t.kv is allocated (one key group), the decode also writes the (key, value) records.
 void sort_full(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_vals, uint64_t nnz,
                int N, const uint64_t* dims, const int* perm, SortedTree& t, PhaseTrace& tr) {
   cudaStream_t st = ctx->stream;
@@ -320,9 +351,12 @@ void sort_full(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
     for (int l = 0; l < N; ++l) ks.src[l] = nullptr;
     ks.lo = 0;
     ks.hi = N;
+    if (t.kv.p)
+      for (int l = 0; l < N; ++l) { t.shift[l] = ks.shift[l]; t.bits[l] = bits[l]; }
     decode_kernel<<<grid, 256, 0, st>>>(ks, BitSet{{bits[0], bits[1], bits[2], bits[3], bits[4],
                                                     bits[5], bits[6], bits[7]}},
-                                        co, nnz, kB.p, order, d_vals, t.vals.p);
+                                        co, nnz, kB.p, order, d_vals, t.vals.p,
+                                        t.kv.p);
   } else {
     gather_kernel<<<grid, 256, 0, st>>>(co, nnz, order, d_vals, t.vals.p);
   }
@@ -433,6 +467,9 @@ void build_csf_set(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* 
     if (roots[k] == Q[0]) qtree = k;
   SortedTree tq;
   alloc_sorted(ctx, tq, nnz, N, out_arena, qtree >= 0);
+  int total_bits = 0;
+  for (int l = 0; l < N; ++l) total_bits += bits_for(dims[l]);
+  if (ntrees > (qtree >= 0 ? 1 : 0) && total_bits <= 64) tq.kv.alloc(nnz, st);
   sort_full(ctx, d_ind, d_vals, nnz, N, dims, Q, tq, tr);
   const int grid = grid_for(ctx, nnz);
   for (int k = 0; k < ntrees; ++k) {
@@ -456,13 +493,24 @@ void build_csf_set(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* 
       SB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, tq.coord[qlev[r]].p,
                                               tr_.coord[0].p, pos.p, perm_out.p, (int)nnz, 0, nb,
                                               st));
-      CoordOut co{};
-      co.N = N;
-      for (int l = 1; l < N; ++l) {
-        co.src[l] = tq.coord[qlev[out.perm[l]]].p;
-        co.dst[l] = tr_.coord[l].p;
+      if (tq.kv.p) {
+        KvOut ko{};
+        ko.N = N;
+        for (int l = 1; l < N; ++l) {
+          ko.dst[l] = tr_.coord[l].p;
+          ko.shift[l] = tq.shift[qlev[out.perm[l]]];
+          ko.bits[l] = tq.bits[qlev[out.perm[l]]];
+        }
+        gather_kv_kernel<<<grid, 256, 0, st>>>(ko, nnz, perm_out.p, tq.kv.p, tr_.vals.p);
+      } else {
+        CoordOut co{};
+        co.N = N;
+        for (int l = 1; l < N; ++l) {
+          co.src[l] = tq.coord[qlev[out.perm[l]]].p;
+          co.dst[l] = tr_.coord[l].p;
+        }
+        gather_levels_kernel<<<grid, 256, 0, st>>>(co, nnz, perm_out.p, tq.vals.p, tr_.vals.p);
       }
-      gather_levels_kernel<<<grid, 256, 0, st>>>(co, nnz, perm_out.p, tq.vals.p, tr_.vals.p);
       SB_CHECK_LAUNCH(ctx);
       tr.mark("derived sort");
     }

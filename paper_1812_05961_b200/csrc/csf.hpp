@@ -35,6 +35,10 @@ struct DevCsf {
   // Non-root MTTKRP: the kHotRows (8) most frequent ids of each level (~0u = unused), computed on
   // first use of that level as an output level.
   uint32_t hot[SPLATT_MAX_NMODES][kHotRows];
+  // ROOT gathers (level 0): -1 not yet timed (L1::no_allocate), 0 L1::no_allocate, 1
+  // L1-allocating.  cpd_als times both on its first two iterations and keeps the faster
+  // (DESIGN.md §4.2); the choice changes no arithmetic.
+  int l1a = -1;
   bool hot_ready[SPLATT_MAX_NMODES] = {false};
   // Leaf-mode tiling for the ROOT MTTKRP: when the leaf factor does
   // not fit in L2, the same tree split by leaf-id range into tiles (each a tree with the same

@@ -141,6 +141,14 @@ int leaf_tiles(splatt_ctx* ctx, const DevCsf& c, int ld) {
   return (int)std::min<double>(8.0, std::ceil(leaf_bytes / budget));
 }
 
+// ROOT gather cache policy: SPLATT_L1_ALLOC=0/1 forces it (A/B runs and
+// tests), else the caller's request, else the tree's timed choice.
+bool l1_allocate(const DevCsf& c, int request) {
+  if (const char* e = getenv("SPLATT_L1_ALLOC")) return *e == '1';
+  if (request >= 0) return request == 1;
+  return c.l1a == 1;
+}
+
 void mttkrp_prepare(splatt_ctx* ctx, DevCsf& c, int level, int ld) {
   if (c.nnz == 0) return;
   if (level == 0) {
@@ -154,7 +162,8 @@ void mttkrp_prepare(splatt_ctx* ctx, DevCsf& c, int level, int ld) {
 }
 
 void mttkrp_level(splatt_ctx* ctx, DevCsf& c, int level, const double* const* fac_by_mode,
-                  double* out, uint64_t out_rows, int ld, int R, EventTimer* tm, int cat) {
+                  double* out, uint64_t out_rows, int ld, int R, EventTimer* tm, int cat,
+                  int l1a_request) {
   if (ld % 4 != 0) fail(SPLATT_ERR_BADINPUT, "internal: ld must be a multiple of 4");
   if (level < 0 || level >= c.N) fail(SPLATT_ERR_BADINPUT, "internal: level out of range");
   if (tm) tm->gap();  // the zero-fill is not part of the timed kernel
@@ -162,7 +171,9 @@ void mttkrp_level(splatt_ctx* ctx, DevCsf& c, int level, const double* const* fa
   if (c.nnz == 0) return;
   const int chunk = mttkrp_chunk_leaves(c.N, ld);
   mttkrp_prepare(ctx, c, level, ld);
+  const int l1a = (level == 0 && l1_allocate(c, l1a_request)) ? 2 : 0;
   auto launch = [&](DevCsf& t, int accumulate) {
+    accumulate |= l1a;
     switch (c.N) {
       case 3: mttkrp_launch_n3(ctx, t, level, fac_by_mode, out, ld, R, chunk, accumulate); break;
       case 4: mttkrp_launch_n4(ctx, t, level, fac_by_mode, out, ld, R, chunk, accumulate); break;
@@ -172,7 +183,7 @@ void mttkrp_level(splatt_ctx* ctx, DevCsf& c, int level, const double* const* fa
       const unsigned blocks = (unsigned)ceil_div(t.nchunks, 8);
       seam_combine_kernel<<<std::max(1u, blocks), 256, 0, ctx->stream>>>(
           t.seam.p, t.tail.p, t.seamrows.p, t.seamrows.p + t.nchunks, t.nchunks, ld, out,
-          accumulate, ctx->d_conv);
+          accumulate & 1, ctx->d_conv);
       SB_CHECK_LAUNCH(ctx);
     }
   };

@@ -10,9 +10,11 @@ namespace sb {
 // (same ld); fac_by_mode[c.perm[level]] is unused.  Zero-fills `out` first (rows without
 // nonzeros are 0).  Stream-ordered on ctx.  If tm is given, only the kernel (not the
 // zero-fill) is timed under category `cat`.
+// l1a: ROOT gather cache policy, -1 = the tree's choice (c.l1a; no_allocate if untimed),
+// 0 = L1::no_allocate, 1 = L1-allocating (env SPLATT_L1_ALLOC=0/1 overrides both).
 void mttkrp_level(splatt_ctx* ctx, DevCsf& c, int level, const double* const* fac_by_mode,
                   double* out, uint64_t out_rows, int ld, int R, EventTimer* tm = nullptr,
-                  int cat = 0);
+                  int cat = 0, int l1a = -1);
 
 // Per-tree MTTKRP metadata for output level `level` (chunk table; for level > 0 the hot
 // output ids), built once; mttkrp_level builds it on first use if this was not called.

@@ -72,13 +72,23 @@ struct Args {
 
 struct d4 { double x, y, z, w; };
 
+// Factor-row gathers.  Default: L1::no_allocate (+2% on c2/c4/c5 in a B200 A/B: the rows
+// stream through L1 without evicting the group tables).  L1A (ROOT kernels whose leaf
+// factor exceeds half the L2, e.g. c3's 138 MB mode-0 factor): L1-allocating, so the
+// power-law hot rows are served from L1 instead of going back to L2 and DRAM (c3 +7.6%;
+// profiles/ab_r01/sweep16.txt).
 #ifndef SB_ROW_LOAD
-#define SB_ROW_LOAD "ld.global.nc.L1::no_allocate.v4.f64"  // +2% vs L1-allocating (B200 A/B)
+#define SB_ROW_LOAD "ld.global.nc.L1::no_allocate.v4.f64"
 #endif
+template <bool L1A = false>
 __device__ __forceinline__ d4 ldg_row(const double* p) {
   d4 r;
-  asm(SB_ROW_LOAD " {%0,%1,%2,%3}, [%4];"
-      : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+  if constexpr (L1A)
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+  else
+    asm(SB_ROW_LOAD " {%0,%1,%2,%3}, [%4];"
+        : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
   return r;
 }
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
@@ -194,7 +204,7 @@ __host__ __device__ constexpr int group_red_doubles(int ld) {
   return D > 0 ? (kRedBufs + kHot) * ld + 2 : 0;
 }
 
-template <int N, int D, int G, int U, int MINB>
+template <int N, int D, int G, int U, int MINB, bool L1A = false>
 __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> a) {
   constexpr int E = Lanes<G>::kE;           // window entries per lane
   constexpr int NB = (D < N - 1) ? (N - 2 - D) : 0;  // bottom-up factor levels D+1..N-2
@@ -288,7 +298,7 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
     if constexpr (NP > 0) {
 #pragma unroll
       for (int l = 0; l < NP; ++l) {
-        const d4 r = ldg_row(a.fac[l] + colc + (size_t)a.ids[l][base[l]] * a.ld);
+        const d4 r = ldg_row<L1A>(a.fac[l] + colc + (size_t)a.ids[l][base[l]] * a.ld);
         Q[l] = (l == 0) ? r : mul4(Q[l > 0 ? l - 1 : 0], r);
       }
     }
@@ -393,15 +403,15 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
           v[u] = sval[t];
           dep[u] = w[1];
           orow[u] = (D == N - 1) ? w[0] : w[2 + (D < N - 1 ? D : 0)];
-          if constexpr (D < N - 1) row[u] = ldg_row(fleaf + (size_t)w[0] * a.ld);
+          if constexpr (D < N - 1) row[u] = ldg_row<L1A>(fleaf + (size_t)w[0] * a.ld);
           const uint32_t d = w[1] & 0xffu;
 #pragma unroll
           for (int l = D + 1; l <= N - 2; ++l)
             if (d <= (uint32_t)l)
-              mid[u][l - D - 1] = ldg_row(a.fac[l] + colc + (size_t)w[2 + l] * a.ld);
+              mid[u][l - D - 1] = ldg_row<L1A>(a.fac[l] + colc + (size_t)w[2 + l] * a.ld);
 #pragma unroll
           for (int l = 0; l < NP; ++l)
-            if (d <= (uint32_t)l) nxt[u][l] = ldg_row(a.fac[l] + colc + (size_t)w[2 + l] * a.ld);
+            if (d <= (uint32_t)l) nxt[u][l] = ldg_row<L1A>(a.fac[l] + colc + (size_t)w[2 + l] * a.ld);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -465,7 +475,7 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
         for (int l = N - 2; l >= 1; --l) {
           if (l < last_dep) {
             const uint32_t nid = a.ids[l][base[l]];
-            const d4 r = ldg_row(a.fac[l] + colc + (size_t)nid * a.ld);
+            const d4 r = ldg_row<L1A>(a.fac[l] + colc + (size_t)nid * a.ld);
             fma4v(acc[l - 1], acc[l], r);
           }
         }
@@ -484,7 +494,7 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
         for (int l = N - 2; l >= D + 1; --l) {
           if (l < last_dep) {
             const uint32_t nid = a.ids[l][base[l]];
-            const d4 r = ldg_row(a.fac[l] + colc + (size_t)nid * a.ld);
+            const d4 r = ldg_row<L1A>(a.fac[l] + colc + (size_t)nid * a.ld);
             fma4v(acc[l - 1], acc[l], r);
           }
         }
@@ -508,7 +518,9 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
   }
 }
 
-template <int N, int D, int G, int U, int MINB>
+// acc: bit 0 = add into the output rows (a later leaf tile), bit 1 = L1-allocating gathers
+// (D = 0 only).
+template <int N, int D, int G, int U, int MINB, bool L1A = false>
 void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, double* out,
               int ld, int R, int chunk, int acc) {
   Args<N> a{};
@@ -531,7 +543,7 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
   a.chunk = (uint32_t)chunk;
   a.ld = (uint32_t)ld;
   a.R = R;
-  a.accumulate = acc;
+  a.accumulate = acc & 1;
   a.conv = ctx->d_conv;
   if (D == 0 && ctx->deterministic) {
     if (c.tail.n < c.nchunks * (size_t)ld) c.tail.alloc(c.nchunks * (size_t)ld, ctx->stream);
@@ -552,7 +564,7 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
   const int groups_per_block = Lanes<G>::groups_per_block(threads);
   const size_t smem = smem_for(threads);
   static const bool attr = [] {  // thread-safe one-time init (loopback ranks are threads)
-    SB_CUDA(cudaFuncSetAttribute(mttkrp_csf_kernel<N, D, G, U, MINB>,
+    SB_CUDA(cudaFuncSetAttribute(mttkrp_csf_kernel<N, D, G, U, MINB, L1A>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     return true;
   }();
@@ -563,12 +575,12 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
     // flushed once per group rather than once per chunk
     int occ = 0;  // depends on ld through the staging rows' shared memory
     SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &occ, mttkrp_csf_kernel<N, D, G, U, MINB>, threads, smem));
+        &occ, mttkrp_csf_kernel<N, D, G, U, MINB, L1A>, threads, smem));
     occ = std::max(occ, 1);
     blocks = std::min<uint64_t>(blocks, (uint64_t)ctx->num_sms * occ);
     for (int h = 0; h < kHotRows; ++h) a.hot[h] = c.hot[D][h];
   }
-  mttkrp_csf_kernel<N, D, G, U, MINB>
+  mttkrp_csf_kernel<N, D, G, U, MINB, L1A>
       <<<(unsigned)std::max<uint64_t>(1, blocks), threads, smem, ctx->stream>>>(a);
   SB_CHECK_LAUNCH(ctx);
 }
@@ -583,9 +595,16 @@ void launch_g(splatt_ctx* ctx, DevCsf& c, const double* const* f, double* out, i
     if (slots <= 2) return launch_t<N, D, 2, U, MB>(ctx, c, f, out, ld, R, chunk, acc);
     if (slots <= 4) return launch_t<N, D, 4, U, MB>(ctx, c, f, out, ld, R, chunk, acc);
 #ifndef SB_MTTKRP_NO_PACK
-    if (D == 0 && (slots == 9 || slots == 10))  // ROOT, R = 33..40: 3 packed groups per warp
+    if (D == 0 && (slots == 9 || slots == 10)) {  // ROOT, R = 33..40: 3 packed groups per warp
+      if (acc & 2) return launch_t<N, D, 10, U, MB, true>(ctx, c, f, out, ld, R, chunk, acc);
       return launch_t<N, D, 10, U, MB>(ctx, c, f, out, ld, R, chunk, acc);
+    }
 #endif
+    if (D == 0 && (acc & 2)) {
+      if (slots <= 8) return launch_t<N, D, 8, U, MB, true>(ctx, c, f, out, ld, R, chunk, acc);
+      if (slots <= 16) return launch_t<N, D, 16, U, MB, true>(ctx, c, f, out, ld, R, chunk, acc);
+      return launch_t<N, D, 32, U, MB, true>(ctx, c, f, out, ld, R, chunk, acc);
+    }
     if (slots <= 16 && slots > 8) return launch_t<N, D, 16, U, MB>(ctx, c, f, out, ld, R, chunk, acc);
   }
   if (slots <= 8) return launch_t<N, D, 8, U, MB>(ctx, c, f, out, ld, R, chunk, acc);

@@ -79,6 +79,31 @@ def test_deterministic_als_bitwise_repeatable(sb):
     als_compare(runs[0], ref)
 
 
+def test_gather_policy_tuning_changes_no_bits(sb, monkeypatch):
+    """cpd_als times the ROOT gathers with L1::no_allocate (iteration 1) and L1-allocating
+    loads (iteration 2) per tree (>= 2^20 nonzeros) and keeps the faster: the choice must not
+    change a bit of the result (deterministic context), whichever way it goes."""
+    t = synth.generate((40_000, 11_000, 75_000), 1_100_000, [("zipf", 1.1)] * 3, "ratings",
+                       seed=23)
+    ctx = sb.Context(0)
+    ctx.set_deterministic(True)
+    ind, vals = dev_coo(t)
+    runs = []
+    for force in (None, "0", "1"):
+        if force is None:
+            monkeypatch.delenv("SPLATT_L1_ALLOC", raising=False)
+        else:
+            monkeypatch.setenv("SPLATT_L1_ALLOC", force)
+        runs.append(sb.cpd_als(ind, vals, t.dims, rank=35, max_iters=5, seed=5, ctx=ctx,
+                               out_device=False, stats=True))
+    for r in runs[1:]:
+        for n in range(3):
+            assert np.array_equal(r["factors"][n].view(np.uint64),
+                                  runs[0]["factors"][n].view(np.uint64))
+        assert np.array_equal(r["lam"].view(np.uint64), runs[0]["lam"].view(np.uint64))
+    assert runs[0]["stats"]["host_syncs"] == runs[1]["stats"]["host_syncs"] + 1  # the tuning sync
+
+
 def test_deterministic_with_leaf_tiles(sb):
     t = synth.generate((60, 50, 300_000), 1_500_000, [("zipf", 1.1), ("uniform",), ("zipf", 1.0)],
                        "ratings", seed=61)

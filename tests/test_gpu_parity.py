@@ -121,6 +121,24 @@ def test_mttkrp_parity_config_shaped(sb, ctx, R):
             assert np.all(M[:, R:] == 0)
 
 
+@pytest.mark.parametrize("R", [8, 35, 64])
+def test_mttkrp_l1_allocating_gathers(sb, ctx, monkeypatch, R):
+    """The ROOT kernels' L1-allocating gather variant (chosen for leaf factors larger than
+    half the L2; forced here with SPLATT_L1_ALLOC=1): same parity bar, N = 3 and 4, packed
+    and power-of-two lane groups."""
+    monkeypatch.setenv("SPLATT_L1_ALLOC", "1")
+    rng = np.random.default_rng(100 + R)
+    for t in (tensors()[1], tensors()[4]):
+        F = [rng.standard_normal((d, R)) for d in t.dims]
+        ind, vals = dev_coo(t)
+        csf = sb.csf_build(ind, vals, t.dims, ctx=ctx)
+        fd = dev_factors(F, ld=sb.padded_ld(R))
+        for n in range(t.nmodes):
+            M = sb.mttkrp(csf, n, fd, rank=R).cpu().numpy()
+            ref = oracle.mttkrp(t.dims, t.ind, t.vals, F, n)
+            assert rel_fro(M[:, :R], ref) <= MTTKRP_TOL, (t.dims, R, n)
+
+
 def test_mttkrp_integer_bit_exact(sb, ctx):
     """X-3: integer values x factors in {0,1,2}: exact in fp64 in any order."""
     rng = np.random.default_rng(11)
