@@ -61,8 +61,10 @@ def gather_view(st, N, R, t_mttkrp, policy):
         return None
     rows = sum(s["iters"] * sum(sum(s["csf_nodes"][n][1:N]) for n in range(N)) for s in st)
     rate = rows / t_mttkrp
-    return {"rows_per_s": rate, "peak_rows_per_s": gp["rows_per_s"],
-            "frac": rate / gp["rows_per_s"], "row_bytes": 8 * ((R + 3) // 4 * 4),
+    row_bytes = 8 * ((R + 3) // 4 * 4)
+    peak = gp.get("rows_per_s_by_row_bytes", {}).get(str(row_bytes))
+    return {"rows_per_s": rate, "peak_rows_per_s": peak,
+            "frac": rate / peak if peak else None, "row_bytes": row_bytes,
             "peak_source": "profiles/gather_peak.json (measured gather microbenchmark)"}
 
 

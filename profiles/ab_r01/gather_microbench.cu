@@ -141,6 +141,48 @@ __global__ void __launch_bounds__(256, 2) gather_flat(const double* __restrict__
   }
 }
 
+
+// ---------------------------------------------------------------- A': LDG lane groups, any ld
+// lanes per row L = ld / 4 (256-bit per lane), 32 / L groups per warp; L1-allocating loads.
+template <int LDX, int U>
+__global__ void __launch_bounds__(256, 3) gather_ldg_w(const double* __restrict__ F,
+                                                       const uint32_t* __restrict__ idx,
+                                                       const double* __restrict__ val,
+                                                       uint64_t nchunks, double* __restrict__ out) {
+  constexpr int L = LDX / 4, GPW = 32 / L;
+  const int lane = threadIdx.x & 31, g = lane / L, gl = lane % L;
+  const bool live = g < GPW;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+  for (uint64_t c0 = warp * GPW; c0 < nchunks; c0 += nwarps * GPW) {
+    const uint64_t c = c0 + g;
+    const bool ok = live && c < nchunks;
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll 1
+    for (int j0 = 0; j0 < 32; j0 += U) {
+      double4 r[U];
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = j0 + u;
+        const uint32_t id = ok ? __ldg(idx + c * 32 + j) : 0u;
+        v[u] = ok ? __ldg(val + c * 32 + j) : 0.0;
+        const double* p = F + (size_t)id * LDX + gl * 4;
+        if (ok)
+          asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                       : "=d"(r[u].x), "=d"(r[u].y), "=d"(r[u].z), "=d"(r[u].w) : "l"(p));
+        else
+          r[u] = make_double4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        a0 += v[u] * r[u].x; a1 += v[u] * r[u].y; a2 += v[u] * r[u].z; a3 += v[u] * r[u].w;
+      }
+    }
+    if (ok) *reinterpret_cast<double4*>(out + c * LDX + gl * 4) = make_double4(a0, a1, a2, a3);
+  }
+}
+
 // ---------------------------------------------------------------- B: TMA gather4
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -343,6 +385,38 @@ int main(int argc, char** argv) {
            name, (unsigned long)I, (unsigned long)(nch * 32), zipf, ms, nch * 32 / (ms * 1e-3),
            nch * 32 * (double)ROWB / (ms * 1e-3) / 1e12, maxerr);
   };
+  if (getenv("WIDTHS")) {
+    // row-gather ceiling by row width (ld = 16 / 36 / 64 doubles), L1-allocating, U = 4
+    for (int w : {16, 36, 64}) {
+      double* Fw;
+      CK(cudaMalloc(&Fw, I * w * 8));
+      CK(cudaMemset(Fw, 0, I * w * 8));
+      double* ow;
+      CK(cudaMalloc(&ow, nch * w * 8));
+      cudaEvent_t x, y;
+      CK(cudaEventCreate(&x));
+      CK(cudaEventCreate(&y));
+      auto run = [&] {
+        if (w == 16) gather_ldg_w<16, 4><<<nsm * 3, 256>>>(Fw, ix, v, nch, ow);
+        if (w == 36) gather_ldg_w<36, 4><<<nsm * 3, 256>>>(Fw, ix, v, nch, ow);
+        if (w == 64) gather_ldg_w<64, 4><<<nsm * 3, 256>>>(Fw, ix, v, nch, ow);
+      };
+      run();
+      CK(cudaDeviceSynchronize());
+      CK(cudaEventRecord(x));
+      for (int i = 0; i < 20; ++i) run();
+      CK(cudaEventRecord(y));
+      CK(cudaEventSynchronize(y));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, x, y));
+      ms /= 20;
+      printf("width ld=%d row_bytes=%d I=%lu zipf=%.2f  %.4f ms  %.3e rows/s\n", w, w * 8,
+             (unsigned long)I, zipf, ms, nch * 32 / (ms * 1e-3));
+      CK(cudaFree(Fw));
+      CK(cudaFree(ow));
+    }
+    return 0;
+  }
   const bool only_ldg = getenv("ONLY_LDG") != nullptr;
   {
     const int blocks = 3;
