@@ -27,8 +27,19 @@ struct Error : std::runtime_error {
                  std::string(#call) + ": " + cudaGetErrorString(e_));                   \
   } while (0)
 
-#define SB_CHECK_LAUNCH(ctx) \
-  do { (ctx)->kernel_launches++; SB_CUDA(cudaGetLastError()); } while (0)
+#define SB_STR2_(x) #x
+#define SB_STR_(x) SB_STR2_(x)
+// Launch check; the message names the launch site (with CUDA_LAUNCH_BLOCKING=1 an
+// asynchronous fault is then attributed to the kernel that caused it).
+#define SB_CHECK_LAUNCH(ctx)                                                            \
+  do {                                                                                  \
+    (ctx)->kernel_launches++;                                                           \
+    cudaError_t e_ = cudaGetLastError();                                                \
+    if (e_ != cudaSuccess)                                                              \
+      ::sb::fail(SPLATT_ERR_CUDA, std::string("kernel launch at " __FILE__ ":"         \
+                                              SB_STR_(__LINE__) ": ") +                 \
+                                      cudaGetErrorString(e_));                          \
+  } while (0)
 
 #define SB_REQUIRE(cond, msg) \
   do { if (!(cond)) ::sb::fail(SPLATT_ERR_BADINPUT, msg); } while (0)

@@ -422,10 +422,12 @@ void finish_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& 
   out.tab.release();
 }
 
-void init_tree(DevCsf& out, int N, uint64_t nnz, const uint64_t* dims, int root) {
+// `arena`: the allocator the tree's arrays come from (nullptr: the stream-ordered pool); the
+// tree's lazily built members (chunk table, seam rows, tiles) are taken from it too.
+void init_tree(DevCsf& out, int N, uint64_t nnz, const uint64_t* dims, int root, Arena* arena) {
   out.N = N;
   out.nnz = nnz;
-  out.arena = current_arena();
+  out.arena = arena;
   csf_perm(N, dims, root, out.perm);
   for (int l = 0; l < N; ++l) {
     out.hot_ready[l] = false;
@@ -452,7 +454,8 @@ void build_csf_set(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* 
   Arena* const out_arena = current_arena();
   if (out_arena && !ctx->arena_scratch) ctx->arena_scratch = new Arena();
   ArenaScope scratch(out_arena ? ctx->arena_scratch : nullptr, true);
-  for (int k = 0; k < ntrees; ++k) init_tree(*outs[k], N, nnz, dims, roots[k]);
+  // (not the scratch arena made current above: the trees outlive this build)
+  for (int k = 0; k < ntrees; ++k) init_tree(*outs[k], N, nnz, dims, roots[k], out_arena);
   // One full sort, in the order Q of all modes by ascending length (the tree rooted at the
   // shortest mode).  Every tree rooted at r has level order (r, Q without r), so its order is
   // a STABLE sort of the Q-ordered nonzeros by their mode-r coordinate alone — a 32-bit key

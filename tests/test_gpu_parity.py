@@ -332,6 +332,12 @@ def test_mttkrp_leaf_tiling(sb, ctx):
         assert rel_fro(M, oracle.mttkrp(t.dims, t.ind, t.vals, F, n)) <= MTTKRP_TOL, n
         Mi = sb.mttkrp(csf, n, fdi, rank=R).cpu().numpy()
         assert np.array_equal(Mi, oracle.mttkrp(t.dims, t.ind, t.vals, Fi, n)), n
-    res = sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=2, seed=3, ctx=ctx)
     ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=R, max_iters=2, seed=3)
-    als_compare(res, ref)
+    # repeated calls on one context: the second call's trees, chunk tables and tiles come
+    # from arenas sized by the first (a tree once recorded the build's scratch arena as its
+    # allocator, so its tiles were released with the build temporaries: illegal access)
+    for _ in range(3):
+        res = sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=2, seed=3, ctx=ctx)
+        als_compare(res, ref)
+    res = sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=5, seed=3, ctx=ctx)  # + gather tuning
+    als_compare(res, oracle.cpd_als(t.dims, t.ind, t.vals, rank=R, max_iters=5, seed=3))
