@@ -238,10 +238,10 @@ def run_reference(args, cfg, t):
     print(json.dumps(line), flush=True)
 
 
-def config_block(cfg, G, policy="all"):
+def config_block(cfg, G, policy="all", leaf_tiling="auto"):
     return {"workload": cfg["name"], "dims": list(cfg["dims"]), "nnz": cfg["nnz"],
             "rank": cfg["rank"], "iters": cfg["iters"], "seed": cfg["seed"],
-            "csf_policy": policy,
+            "csf_policy": policy, "leaf_tiling": leaf_tiling,
             "parallelism": (f"root-mode partitioned x{G} (P1/P2 per mode)" if G > 1 else "single GPU"),
             "l2": "inputs larger than L2 (COO + per-mode CSFs >> 126 MB); no explicit flush"}
 
@@ -262,8 +262,9 @@ def main():
                     help="seconds between clock samples")
     ap.add_argument("--policy", default="all", choices=["all", "one", "two"],
                     help="CSF allocation policy (SPLATT_CSF_*)")
-    ap.add_argument("--leaf-tiling", type=float, default=0.0,
-                    help="ROOT MTTKRP leaf tiling above this fraction of L2 (0 = off)")
+    ap.add_argument("--leaf-tiling", default="auto",
+                    help="ROOT MTTKRP leaf tiling above this fraction of L2 (0 = off; default "
+                         "auto = the library's: half-L2 tiles in runs of >= 10 iterations)")
     ap.add_argument("--partition", default="auto", choices=["auto", "nnz", "slices"],
                     help="multi-GPU split: per-mode auto, equal nonzero ranges (P2), whole slices (P1)")
     args = ap.parse_args()
@@ -296,8 +297,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     stream = torch.cuda.Stream(local)
     ctx = sb.Context(local, stream=stream)
-    if args.leaf_tiling > 0:
-        ctx.set_leaf_tiling(args.leaf_tiling)
+    if args.leaf_tiling != "auto":
+        ctx.set_leaf_tiling(float(args.leaf_tiling))
     if world > 1:
         ctx.set_comm()
         ctx.set_partition(args.partition)
@@ -415,7 +416,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_block(cfg, world, args.policy),
+        "config": config_block(cfg, world, args.policy, args.leaf_tiling),
         "cpals_sec_per_iter": statistics.mean(loop) / iters,
         "mttkrp_nnzR_per_s": N * t.nnz * R * iters * args.steps / t_mttkrp if t_mttkrp else None,
         "breakdown_s_per_step": {k: sum(s[k] for s in st) / args.steps for k in

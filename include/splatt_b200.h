@@ -212,9 +212,13 @@ splatt_status splatt_ctx_set_deterministic(splatt_ctx* ctx, int32_t on);
  * the MTTKRP runs with) into T = ceil(bytes / (l2_fraction x L2)) trees by leaf-id range,
  * run one after another (later tiles add into the owned rows), so each tile's leaf rows
  * stay in L2.  It trades DRAM misses for split fibers (more internal-node gathers) and a
- * one-time split costing about one CSF build: on c3 (480k-row leaf factor, 138 MB) MTTKRP
- * drops ~6%, so it pays only for long runs.  0 (default) = off.
- * Errors: BADINPUT (negative or > 4).                                                    */
+ * one-time split (c3: ~5 ms per tree, 100M nonzeros): on c3 (480k-row leaf factor,
+ * 138 MB) the 20-iteration ALS MTTKRP drops 269 -> 247 ms.
+ * l2_fraction = SPLATT_LEAF_TILING_AUTO (the default): tiles of half the L2 inside
+ * splatt_cpd_als* runs of >= 10 iterations (where the split pays for itself), none for a
+ * single splatt_mttkrp; 0 = off; > 0 = always, at that fraction.
+ * Errors: BADINPUT (> 4, or negative other than AUTO).                                  */
+#define SPLATT_LEAF_TILING_AUTO (-1.0)
 splatt_status splatt_ctx_set_leaf_tiling(splatt_ctx* ctx, double l2_fraction);
 
 /* ---------------------------------------------------------------- CSF */

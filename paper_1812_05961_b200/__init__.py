@@ -23,7 +23,7 @@ __all__ = ["lib", "Context", "Loopback", "Csf", "csf_build", "mttkrp", "cpd_als"
            "partition",
            "Tensor", "read_tns", "write_tns", "coo_stats",
            "SplattError", "SingularError", "EmptyTensorError", "STATUS", "padded_ld",
-           "CSF_ALL", "CSF_ONE", "CSF_TWO", "POLICIES"]
+           "CSF_ALL", "CSF_ONE", "CSF_TWO", "POLICIES", "LEAF_TILING_AUTO"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SPLATT_B200_LIB") or os.path.join(_HERE, "libsplatt_b200.so")
@@ -33,6 +33,7 @@ CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
 
 CSF_ALL, CSF_ONE, CSF_TWO = 0, 1, 2  # SPLATT_CSF_* (include/splatt_b200.h)
 POLICIES = {"all": CSF_ALL, "one": CSF_ONE, "two": CSF_TWO}
+LEAF_TILING_AUTO = -1.0  # SPLATT_LEAF_TILING_AUTO
 
 STATUS = {0: "OK", -1: "BADINPUT", -2: "NOMEM", -3: "SINGULAR", -4: "CUDA", -5: "NCCL",
           -6: "EMPTY", -7: "UNSUPPORTED"}
@@ -238,9 +239,12 @@ class Context:
         """Bitwise-reproducible ROOT MTTKRP (fixed-order chunk-seam sums instead of atomics)."""
         _raise(lib().splatt_ctx_set_deterministic(self._p, 1 if on else 0), self._p)
 
-    def set_leaf_tiling(self, l2_fraction: float = 0.5):
-        """Enable ROOT-MTTKRP leaf tiling for leaf factors above l2_fraction x L2 (0 = off)."""
-        _raise(lib().splatt_ctx_set_leaf_tiling(self._p, float(l2_fraction)), self._p)
+    def set_leaf_tiling(self, l2_fraction=0.5):
+        """ROOT-MTTKRP leaf tiling for leaf factors above l2_fraction x L2: a fraction > 0
+        (always), 0 (off) or "auto" (the default: half-L2 tiles in ALS runs of >= 10
+        iterations)."""
+        f = LEAF_TILING_AUTO if l2_fraction == "auto" else float(l2_fraction)
+        _raise(lib().splatt_ctx_set_leaf_tiling(self._p, f), self._p)
 
     def set_comm_loopback(self, group: "Loopback", rank: int):
         """Join an in-process loopback group as logical rank `rank` (testing the sharded

@@ -198,7 +198,9 @@ splatt_status splatt_ctx_set_deterministic(splatt_ctx* ctx, int32_t on) {
 }
 
 splatt_status splatt_ctx_set_leaf_tiling(splatt_ctx* ctx, double l2_fraction) {
-  if (!ctx || !(l2_fraction >= 0.0) || l2_fraction > 4.0) return SPLATT_ERR_BADINPUT;
+  if (!ctx || !(l2_fraction >= 0.0 || l2_fraction == SPLATT_LEAF_TILING_AUTO) ||
+      l2_fraction > 4.0)
+    return SPLATT_ERR_BADINPUT;
   ctx->leaf_tile_frac = l2_fraction;
   return SPLATT_OK;
 }

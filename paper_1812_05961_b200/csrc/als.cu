@@ -194,6 +194,14 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   ctx->arena_call->reset();
   ctx->arena_scratch->reset();
   ArenaScope call_scope(ctx->arena_call, false);
+  // Leaf tiling AUTO (splatt_ctx_set_leaf_tiling): half-L2 tiles for runs of >= 10
+  // iterations, where the one-time split pays for itself; restored on return.
+  struct TileMode {
+    splatt_ctx* c;
+    double saved;
+    ~TileMode() { c->leaf_tile_frac = saved; }
+  } tile_mode{ctx, ctx->leaf_tile_frac};
+  if (ctx->leaf_tile_frac < 0.0) ctx->leaf_tile_frac = max_iters >= 10 ? 0.5 : 0.0;
   uint64_t launches0 = ctx->kernel_launches;
   const uint64_t syncs0 = ctx->host_syncs;
   const double sync_s0 = ctx->host_sync_s;

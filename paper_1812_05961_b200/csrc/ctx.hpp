@@ -41,7 +41,7 @@ struct splatt_ctx {
   std::string err;
   uint64_t kernel_launches = 0;
   int part_mode = SPLATT_PART_AUTO;    // sharded path: P1 / P2 per mode (SPLATT_PART_*)
-  double leaf_tile_frac = 0.0;         // ROOT MTTKRP leaf tiling (0 = off)
+  double leaf_tile_frac = -1.0;        // ROOT MTTKRP leaf tiling (0 = off, < 0 = auto)
   bool deterministic = false;          // ROOT MTTKRP seams: fixed-order sums, no atomics
   // During an ALS call with tol > 0: device int, the iteration at which the fit stopped
   // improving (0 = still running).  Kernels of the loop return at once when it is set, so

@@ -133,7 +133,7 @@ __global__ void seam_combine_kernel(const double* __restrict__ head, const doubl
 // context enables them (splatt_ctx_set_leaf_tiling): T tiles of at most `leaf_tile_frac` of
 // the L2 capacity each.
 int leaf_tiles(splatt_ctx* ctx, const DevCsf& c, int ld) {
-  const double frac = ctx->leaf_tile_frac;
+  const double frac = ctx->leaf_tile_frac;  // auto (< 0) outside an ALS run: off
   if (!(frac > 0.0)) return 1;
   const double leaf_bytes = (double)c.dims[c.N - 1] * ld * 8.0;
   const double budget = frac * (double)(ctx->l2_bytes ? ctx->l2_bytes : (126u << 20));

@@ -121,6 +121,26 @@ def test_mttkrp_parity_config_shaped(sb, ctx, R):
             assert np.all(M[:, R:] == 0)
 
 
+def test_leaf_tiling_auto_in_long_als_runs(sb):
+    """Leaf tiling AUTO (the default): ALS runs of >= 10 iterations tile ROOT trees whose leaf
+    factor exceeds half the L2 (300k x 36 doubles = 86 MB -> 2 tiles) — same result as the
+    oracle; a second call on the context reuses arenas sized by the first."""
+    t = synth.generate((60, 50, 300_000), 1_500_000, [("zipf", 1.1), ("uniform",), ("zipf", 1.0)],
+                       "ratings", seed=62)
+    ind, vals = dev_coo(t)
+    ctx = sb.Context(0)
+    ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=35, max_iters=10, seed=4)
+    for _ in range(2):
+        res = sb.cpd_als(ind, vals, t.dims, rank=35, max_iters=10, seed=4, ctx=ctx, stats=True)
+        als_compare(res, ref)
+    off = sb.Context(0)
+    off.set_leaf_tiling(0)
+    res_off = sb.cpd_als(ind, vals, t.dims, rank=35, max_iters=10, seed=4, ctx=off, stats=True)
+    als_compare(res_off, ref)
+    # the tiled tree runs one ROOT launch per tile (and its split kernels) where off runs one
+    assert res["stats"]["kernel_launches"] > res_off["stats"]["kernel_launches"]
+
+
 @pytest.mark.parametrize("R", [8, 35, 64])
 def test_mttkrp_l1_allocating_gathers(sb, ctx, monkeypatch, R):
     """The ROOT kernels' L1-allocating gather variant (chosen for leaf factors larger than
@@ -324,6 +344,9 @@ def test_mttkrp_leaf_tiling(sb, ctx):
     Fi = [rng.integers(0, 3, (d, R)).astype(np.float64) for d in t.dims]
     ind, vals = dev_coo(t)
     ctx = sb.Context(0)
+    with pytest.raises(sb.BadInputError):
+        ctx.set_leaf_tiling(-0.5)
+    ctx.set_leaf_tiling("auto")
     ctx.set_leaf_tiling(0.5)
     csf = sb.csf_build(ind, vals, t.dims, ctx=ctx)
     fd, fdi = dev_factors(F), dev_factors(Fi)
