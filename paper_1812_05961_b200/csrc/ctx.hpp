@@ -58,7 +58,26 @@ struct splatt_ctx {
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_aux = nullptr;
   std::unique_ptr<sb::Comm> comm;
+  // Pinned host staging for the call's small device->host results (status words, fit
+  // history): async copies, so the host can collect timings while the device finishes.
+  char* h_pinned = nullptr;
+  size_t h_pinned_bytes = 0;
+  char* pinned(size_t bytes) {
+    if (bytes > h_pinned_bytes) {
+      if (h_pinned) cudaFreeHost(h_pinned);
+      h_pinned = nullptr;
+      h_pinned_bytes = 0;
+      const size_t want = std::max<size_t>(bytes, 4096);
+      if (cudaHostAlloc((void**)&h_pinned, want, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+      }
+      h_pinned_bytes = want;
+    }
+    return h_pinned;
+  }
   ~splatt_ctx() {
+    if (h_pinned) cudaFreeHost(h_pinned);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_pool_aux) cudaEventDestroy(e);
     if (ev_ready) cudaEventDestroy(ev_ready);
@@ -232,9 +251,25 @@ struct EventTimer {
   }
   // Any stream work between end() and the next begin() must not be attributed: call gap().
   void gap() { last_end = -1; }
-  // Requires the stream to have completed.
+  // Spans complete in enqueue order (one stream): collect_ready() adds those whose end event
+  // has completed (non-blocking; callable while the device still runs), collect() the rest
+  // (requires the stream to have completed).
+  size_t cursor = 0;
+  void collect_ready(double* per_cat, int ncat) {
+    for (; cursor < spans.size(); ++cursor) {
+      const Span& sp = spans[cursor];
+      if (cudaEventQuery((*pool)[sp.b]) != cudaSuccess) {
+        cudaGetLastError();  // cudaErrorNotReady is not an error
+        return;
+      }
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, (*pool)[sp.a], (*pool)[sp.b]) == cudaSuccess && sp.cat < ncat)
+        per_cat[sp.cat] += ms * 1e-3;
+    }
+  }
   void collect(double* per_cat, int ncat) {
-    for (auto& sp : spans) {
+    for (; cursor < spans.size(); ++cursor) {
+      const Span& sp = spans[cursor];
       float ms = 0.f;
       if (cudaEventElapsedTime(&ms, (*pool)[sp.a], (*pool)[sp.b]) == cudaSuccess && sp.cat < ncat)
         per_cat[sp.cat] += ms * 1e-3;
