@@ -26,13 +26,14 @@ void mttkrp_launch_n3(splatt_ctx* ctx, DevCsf& c, int D, const double* const* f,
   }
 }
 
-// Leaves per work unit (measured on B200: c2/c4 best at 256 for N = 3, c5 at 512 for N = 4;
-// shorter chunks balance better, longer ones amortise the per-chunk setup and seam rows).
+// Leaves per work unit (measured on B200: c2/c4 best at 256 for N = 3, c5 at 1024 for N = 4
+// (+1.8% over 512, 2048 +1.3%; profiles/ab_r01/sweep17.txt); shorter chunks balance better,
+// longer ones amortise the per-chunk setup and seam rows).
 #ifndef SB_MTTKRP_CHUNK3
 #define SB_MTTKRP_CHUNK3 256
 #endif
 #ifndef SB_MTTKRP_CHUNK
-#define SB_MTTKRP_CHUNK 512
+#define SB_MTTKRP_CHUNK 1024
 #endif
 
 int mttkrp_chunk_leaves(int N, int ld) {

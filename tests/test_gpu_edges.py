@@ -70,9 +70,11 @@ def test_max_rank_128(sb, ctx, policy):
     als_compare(res, ref)
 
 
-@pytest.mark.parametrize("nnz", [255, 256, 257, 511, 512, 513, 4095, 4096, 4097])
+@pytest.mark.parametrize("nnz", [255, 256, 257, 511, 512, 513, 1023, 1024, 1025, 4095, 4096,
+                                 4097])
 def test_chunk_boundaries(sb, ctx, nnz):
-    """nnz around the leaf-chunk sizes (256 for 3 modes, 512 for 4) and the 32-leaf batches:
+    """nnz around the leaf-chunk sizes (256 for 3 modes, 1024 for 4+; 512 the non-root
+    kernels' power-of-two groups see) and the 32-leaf batches:
     ragged last chunk, exactly full chunks, one leaf past."""
     for N in (3, 4):
         t = synth.generate((60, 50, 40, 30)[:N], nnz, [("zipf", 1.2)] * N, "u01", seed=nnz + N)
@@ -102,3 +104,32 @@ def test_repeated_calls_reuse_arena(sb, ctx):
         res = sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=3, seed=seed, ctx=ctx)
         ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=R, max_iters=3, seed=seed)
         als_compare(res, ref)
+
+
+@pytest.mark.parametrize("policy", ["all", "one", "two"])
+def test_csf_maximum_dims(sb, ctx, policy):
+    """Maximum mode lengths (I < 2^32: 32-bit coordinates, a 65-bit composite key -> two
+    key groups; coordinates at 0 and I - 1 included) and duplicates: every tree bit-exact
+    against the oracle.  (MTTKRP at these lengths would need 2^32-row factors.)"""
+    rng = np.random.default_rng(71)
+    dims = (2**32 - 1, 2**31 + 5, 7)
+    n = 3000
+    ind = [rng.integers(0, d, n, dtype=np.uint64).astype(np.uint32) for d in dims]
+    ind[0][:3] = [0, dims[0] - 1, dims[0] - 1]
+    ind[1][:3] = [dims[1] - 1, 0, 0]
+    ind[2][:3] = [6, 0, 0]                       # positions 1 and 2: a duplicate pair
+    t = synth.SparseTensor(dims, ind, rng.random(n))
+    dind, dvals = dev_coo(t)
+    csf = sb.csf_build(dind, dvals, t.dims, ctx=ctx, policy=policy)
+    for k in range(csf.ncsf):
+        g = csf.export(k)
+        o = oracle.csf_build(t.dims, t.ind, t.vals, g["perm"][0])
+        assert g["perm"] == o["perm"].tolist()
+        for l in range(3):
+            assert np.array_equal(g["ids"][l], o["ids"][l]), (k, l)
+        for l in range(2):
+            assert np.array_equal(g["ptr"][l], o["ptr"][l]), (k, l)
+        assert np.array_equal(g["vals"].view(np.uint64), o["vals"].view(np.uint64))
+    bad = [a.clone() for a in dind]
+    with pytest.raises(sb.BadInputError):
+        sb.csf_build(bad, dvals, (2**32, dims[1], dims[2]), ctx=ctx, policy=policy)
