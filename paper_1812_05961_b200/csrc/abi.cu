@@ -71,12 +71,16 @@ void check_coo(const splatt_coo* coo) {
   if (coo->nnz >= (1ull << 31)) fail(SPLATT_ERR_UNSUPPORTED, "nnz >= 2^31 not supported");
 }
 
-// Device view of a caller COO; host arrays are uploaded into owned buffers.
+// Device view of a caller COO; host arrays are uploaded into owned buffers.  Host values
+// go up on the context's copy stream, so their upload overlaps the index upload, the
+// validation and the sort; the first kernel that reads them waits (sb::wait_vals).
 struct StagedCoo {
   DevCoo view;
   DevBuf<uint32_t> ind[SPLATT_MAX_NMODES];
   DevBuf<double> vals;
-  StagedCoo(splatt_ctx* ctx, const splatt_coo* coo) {
+  splatt_ctx* ctx_ = nullptr;
+  ~StagedCoo() { if (ctx_) { try { wait_vals(ctx_); } catch (...) {} } }  // before the free
+  StagedCoo(splatt_ctx* ctx, const splatt_coo* coo) : ctx_(ctx) {
     view.N = coo->nmodes;
     view.nnz = coo->nnz;
     for (int m = 0; m < coo->nmodes; ++m) {
@@ -94,8 +98,13 @@ struct StagedCoo {
       view.vals = coo->vals;
     } else {
       vals.alloc(coo->nnz, ctx->stream);
+      ctx->ensure_copy();
+      SB_CUDA(cudaEventRecord(ctx->ev_copy_start, ctx->stream));  // after the allocation
+      SB_CUDA(cudaStreamWaitEvent(ctx->copy, ctx->ev_copy_start, 0));
       SB_CUDA(cudaMemcpyAsync(vals.p, coo->vals, coo->nnz * 8, cudaMemcpyHostToDevice,
-                              ctx->stream));
+                              ctx->copy));
+      SB_CUDA(cudaEventRecord(ctx->ev_vals, ctx->copy));
+      ctx->vals_pending = true;
       view.vals = vals.p;
     }
     if (getenv("SPLATT_DEBUG_STAGING")) {

@@ -221,16 +221,22 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   if (!prebuilt) validate_coo_enqueue(ctx, X.ind, X.nnz, N, X.dims, bad.p);
   DevBuf<double> normx(1, s);
   // ||X||^2 from the COO values, or from the leaf values of a prebuilt tree (the same
-  // numbers in another order: the sum differs by rounding only)
-  norm_sq(ctx, prebuilt ? prebuilt->csf[0]->vals.p : X.vals, X.nnz, normx.p);
+  // numbers in another order: the sum differs by rounding only).  Unsharded with host-staged
+  // values, it is taken after the build instead (the upload overlaps the sort) and checked
+  // at the end of the call (EMPTY then takes precedence over the other statuses).
+  const bool late_norm = !sharded && !prebuilt && ctx->vals_pending;
   double h_normx = 0.0;
   int h_bad = 0;
-  SB_CUDA(cudaMemcpyAsync(&h_normx, normx.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (!late_norm) {
+    wait_vals(ctx);
+    norm_sq(ctx, prebuilt ? prebuilt->csf[0]->vals.p : X.vals, X.nnz, normx.p);
+    SB_CUDA(cudaMemcpyAsync(&h_normx, normx.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+  }
   SB_CUDA(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   host_sync(ctx);
   if (h_bad) fail(SPLATT_ERR_BADINPUT, "index out of range for its mode");
   tr.mark("validate");
-  if (!(h_normx > 0.0)) fail(SPLATT_ERR_EMPTY, "||X|| = 0");
+  if (!late_norm && !(h_normx > 0.0)) fail(SPLATT_ERR_EMPTY, "||X|| = 0");
 
   // ------------------------------------------- partition + CSF build per mode
   // Unsharded: the policy's CSFs (ALL / ONE / TWO); mode n runs its MTTKRP on
@@ -263,6 +269,10 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       csf[k] = owned[k].get();
     }
     build_csf_set(ctx, X.ind, X.vals, X.nnz, N, X.dims, roots, ncsf, csf.data());
+    if (late_norm) {
+      wait_vals(ctx);  // (the build's decode already did)
+      norm_sq(ctx, X.vals, X.nnz, normx.p);
+    }
   }
   for (int n = 0; n < N && sharded; ++n) {
     owned[n] = std::make_unique<DevCsf>();
@@ -592,6 +602,9 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   double* p_hist = pin ? reinterpret_cast<double*>(pin + 2 * sizeof(double)) : nullptr;
   SB_CUDA(cudaMemcpyAsync(p_sc ? p_sc : &h_status, status.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   SB_CUDA(cudaMemcpyAsync(p_sc ? p_sc + 1 : &h_conv, conv.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  double* p_normx = pin ? reinterpret_cast<double*>(pin + sizeof(double)) : &h_normx;
+  if (late_norm)
+    SB_CUDA(cudaMemcpyAsync(p_normx, normx.p, sizeof(double), cudaMemcpyDeviceToHost, s));
   SB_CUDA(cudaMemcpyAsync(p_hist ? p_hist : h_hist.data(), fit_hist.p, max_iters * sizeof(double),
                           cudaMemcpyDeviceToHost, s));
   if (st) SB_CUDA(cudaEventRecord(call_b, s));
@@ -613,6 +626,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     h_conv = p_sc[1];
     std::copy(p_hist, p_hist + max_iters, h_hist.begin());
   }
+  if (late_norm) h_normx = *p_normx;
   float loop_ms = 0.f;
   cudaEventElapsedTime(&loop_ms, loop_a, loop_b);
   cudaEventDestroy(loop_a);
@@ -623,6 +637,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     cudaEventDestroy(call_a);
     cudaEventDestroy(call_b);
   }
+  if (late_norm && !(h_normx > 0.0)) fail(SPLATT_ERR_EMPTY, "||X|| = 0");
   if (h_status) fail(SPLATT_ERR_SINGULAR, "Gram Hadamard product is singular (after ridge)");
   if (h_conv) it_done = h_conv;  // later enqueued iterations were no-ops
   *out.fit = h_hist[it_done - 1];

@@ -344,6 +344,7 @@ void sort_full(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
     co.src[l] = lvl_src[l];
     co.dst[l] = t.coord[l].p;
   }
+  wait_vals(ctx);  // a host-staged value upload overlapped the sort
   if (groups.size() == 1) {
     KeySpec ks{};
     int sh = 0;

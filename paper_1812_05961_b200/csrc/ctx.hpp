@@ -57,6 +57,11 @@ struct splatt_ctx {
   // fit) and two ordering events; created on first use, owned by the context.
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_aux = nullptr;
+  // Host-staged COO values: uploaded on `copy` (overlapping the index upload and the sort);
+  // ev_vals marks the end of the upload while vals_pending (sb::wait_vals).
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_copy_start = nullptr, ev_vals = nullptr;
+  bool vals_pending = false;
   std::unique_ptr<sb::Comm> comm;
   // Pinned host staging for the call's small device->host results (status words, fit
   // history): async copies, so the host can collect timings while the device finishes.
@@ -83,9 +88,18 @@ struct splatt_ctx {
     if (ev_ready) cudaEventDestroy(ev_ready);
     if (ev_aux) cudaEventDestroy(ev_aux);
     if (aux) cudaStreamDestroy(aux);
+    if (ev_copy_start) cudaEventDestroy(ev_copy_start);
+    if (ev_vals) cudaEventDestroy(ev_vals);
+    if (copy) cudaStreamDestroy(copy);
     delete_arenas();
   }
   void delete_arenas();
+  void ensure_copy() {
+    if (copy) return;
+    SB_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+    SB_CUDA(cudaEventCreateWithFlags(&ev_copy_start, cudaEventDisableTiming));
+    SB_CUDA(cudaEventCreateWithFlags(&ev_vals, cudaEventDisableTiming));
+  }
   void ensure_aux() {
     if (aux) return;
     SB_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
@@ -302,6 +316,14 @@ struct PhaseTrace {
 };
 
 // Blocking wait on the context stream, counted and timed (splatt_stats host_syncs).
+// Order the context stream after a pending host->device upload of the COO values (no-op
+// otherwise).  Called right before the first kernel that reads the values.
+inline void wait_vals(splatt_ctx* ctx) {
+  if (!ctx->vals_pending) return;
+  SB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_vals, 0));
+  ctx->vals_pending = false;
+}
+
 inline void host_sync(splatt_ctx* ctx) {
   const auto t0 = std::chrono::steady_clock::now();
   SB_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -320,6 +320,13 @@ def test_errors(sb, ctx):
         sb.cpd_als(ind, vals, t.dims, rank=2, max_iters=0, ctx=ctx)
     with pytest.raises(sb.EmptyTensorError):
         sb.cpd_als(ind, vals * 0, t.dims, rank=2, max_iters=1, ctx=ctx)
+    # host-staged values (uploaded while the sort runs; ||X|| checked at the end of the call)
+    with pytest.raises(sb.EmptyTensorError):
+        sb.cpd_als(t.ind, t.vals * 0, t.dims, rank=2, max_iters=3, ctx=ctx, out_device=False)
+    bad_host = [a.copy() for a in t.ind]
+    bad_host[2][-1] = t.dims[2]
+    with pytest.raises(sb.BadInputError):
+        sb.cpd_als(bad_host, t.vals, t.dims, rank=2, max_iters=1, ctx=ctx, out_device=False)
     bad = [a.clone() for a in ind]
     bad[1][0] = t.dims[1]
     with pytest.raises(sb.BadInputError):
