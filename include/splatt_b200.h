@@ -102,7 +102,8 @@ typedef struct {
   double   t_mttkrp;        /* all MTTKRP launches (incl. output zeroing)               */
   double   t_build;         /* validation + COO->CSF build ("Sort")                     */
   double   t_ata;           /* Hadamard of Grams + Gram refresh ("Mat A^TA")           */
-  double   t_norm;          /* lambda + column scaling ("Mat norm")                     */
+  double   t_norm;          /* partial reduction + lambda ("Mat norm"); one rank: on the  */
+                            /*   side stream, overlapped with the next MTTKRP             */
   double   t_fit;           /* fit ("CPD fit")                                          */
   double   t_inverse;       /* Cholesky + row solves ("Inverse")                        */
   double   t_comm;          /* NCCL collectives (0 on one GPU)                          */

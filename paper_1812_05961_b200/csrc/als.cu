@@ -412,6 +412,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   tm.end();
 
   // ----------------------------------------------------------------- loop
+  DevBuf<double> rpart(rows_partials_cap(ctx, R), s);  // per-CTA solve partials (RowsReduce)
   double mttkrp_bytes = 0.0, mttkrp_min = 0.0;
   uint64_t mttkrp_launches = 0;
   // Rows of each mode a launch can reference, for the compulsory-traffic figure: the root
@@ -538,9 +539,13 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       // (line 6); sharded: the statistics are all-reduced first.
       const LambdaOut lo_fused{it == 1, lambda.p, Gall.p + n * RR, inner.p, sig.p + (size_t)n * R,
                                ticket.p};
+      // single rank: the reduction + lambda step runs on the side stream, overlapping the
+      // next mode's MTTKRP (which reads the stored factor rows, not lambda or the Grams)
+      const RowsReduce rr{aux, ctx->ev_solved, rpart.p, rpart.n, &tma, kNorm};
       tm.begin(kInverse);
       rows_solve_stats(ctx, M.p, A[n].p, lo, hi, R, ld, Vinv.p, tau.p, true, n == N - 1,
-                       status.p, stats.p, sharded ? nullptr : &lo_fused);
+                       status.p, stats.p, sharded ? nullptr : &lo_fused,
+                       sharded ? nullptr : &rr);
       tm.end();
       if (sharded) {
         tm.begin(kComm);
@@ -655,7 +660,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     st->t_mttkrp = t[kMttkrp];
     st->t_build = t[kBuild];
     st->t_ata = t[kAta];
-    st->t_norm = t[kNorm];
+    st->t_norm = t[kNorm] + ta[kNorm];  // single rank: on the side stream (overlapped)
     st->t_fit = t[kFit];
     st->t_inverse = t[kInverse];
     st->t_comm = t[kComm];

@@ -56,7 +56,7 @@ struct splatt_ctx {
   // Side stream for the R x R work that overlaps the MTTKRP (V^-1 of the next mode, the
   // fit) and two ordering events; created on first use, owned by the context.
   cudaStream_t aux = nullptr;
-  cudaEvent_t ev_ready = nullptr, ev_aux = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_aux = nullptr, ev_solved = nullptr;
   // Host-staged COO values: uploaded on `copy` (overlapping the index upload and the sort);
   // ev_vals marks the end of the upload while vals_pending (sb::wait_vals).
   cudaStream_t copy = nullptr;
@@ -87,6 +87,7 @@ struct splatt_ctx {
     for (cudaEvent_t e : ev_pool_aux) cudaEventDestroy(e);
     if (ev_ready) cudaEventDestroy(ev_ready);
     if (ev_aux) cudaEventDestroy(ev_aux);
+    if (ev_solved) cudaEventDestroy(ev_solved);
     if (aux) cudaStreamDestroy(aux);
     if (ev_copy_start) cudaEventDestroy(ev_copy_start);
     if (ev_vals) cudaEventDestroy(ev_vals);
@@ -105,6 +106,7 @@ struct splatt_ctx {
     SB_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
     SB_CUDA(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
     SB_CUDA(cudaEventCreateWithFlags(&ev_aux, cudaEventDisableTiming));
+    SB_CUDA(cudaEventCreateWithFlags(&ev_solved, cudaEventDisableTiming));
   }
 };
 

@@ -856,9 +856,8 @@ void launch_rows_mma(int NT, const RowsArgs& a, int P, size_t smem, cudaStream_t
 // Fixed-order reduction of the P per-CTA partials (with the lambda / G_n step fused when
 // `fuse` is given).
 void reduce_rows_stats(splatt_ctx* ctx, const double* part, int P, int R, double* stats,
-                       const LambdaOut* fuse) {
+                       const LambdaOut* fuse, cudaStream_t s) {
   const size_t SL = stats_len(R);
-  cudaStream_t s = ctx->stream;
   const unsigned rblocks = (unsigned)ceil_div(SL, kThreads / 32);
   if (fuse) {
     reduce_lambda_kernel<<<rblocks, kThreads, R * sizeof(double), s>>>(
@@ -879,7 +878,8 @@ bool getenv_flag(const char* name) {
 
 void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, uint64_t hi,
                       int R, int ld, const double* Vinv, const double* tau, bool solve,
-                      bool inner, const int* status, double* stats, const LambdaOut* fuse) {
+                      bool inner, const int* status, double* stats, const LambdaOut* fuse,
+                      const RowsReduce* rr) {
   // Vinv: ld x ld, zero pads (hadamard_inverse)
   (void)inner;  // the inner product is always produced by the solve (it is free)
   const size_t SL = stats_len(R);
@@ -888,6 +888,27 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
     SB_CUDA(cudaMemsetAsync(stats, 0, SL * sizeof(double), s));
     return;
   }
+  // The fixed-order reduction of the per-CTA partials: on this stream, or (rr) on another
+  // stream after an event, from rr's persistent partial buffer.
+  auto reduce = [&](const double* part, int P) {
+    if (rr && part == rr->part) {
+      SB_CUDA(cudaEventRecord(rr->ev, s));
+      SB_CUDA(cudaStreamWaitEvent(rr->stream, rr->ev, 0));
+      if (rr->tm) {
+        rr->tm->gap();  // the span starts once the solve is done, not at the last aux span
+        rr->tm->begin(rr->cat);
+      }
+      reduce_rows_stats(ctx, part, P, R, stats, fuse, rr->stream);
+      if (rr->tm) rr->tm->end();
+    } else {
+      reduce_rows_stats(ctx, part, P, R, stats, fuse, s);
+    }
+  };
+  auto part_for = [&](DevBuf<double>& own, int P) -> double* {
+    if (rr && (size_t)P * SL <= rr->cap) return rr->part;
+    own.alloc((size_t)P * SL, s);
+    return own.p;
+  };
   const int ldp = ld + 2;
   const int slots = ld / 4;
   const int G = slots <= 2 ? 2 : slots <= 4 ? 4 : slots <= 8 ? 8 : slots <= 16 ? 16 : 32;
@@ -937,21 +958,25 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
     const int Pm = (int)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(nslabs, W),
                                                                  (uint64_t)ctx->num_sms));
     ArenaScope scratch(current_arena() ? ctx->arena_scratch : nullptr, true);  // per-launch
-    DevBuf<double> part((size_t)Pm * SL, s);
-    a.part = part.p;
+    DevBuf<double> own;
+    a.part = part_for(own, Pm);
     launch_rows_mma(NT, a, Pm, msmem, s);
     SB_CHECK_LAUNCH(ctx);
-    reduce_rows_stats(ctx, part.p, Pm, R, stats, fuse);
+    reduce(a.part, Pm);
     return;
   }
   ArenaScope scratch(current_arena() ? ctx->arena_scratch : nullptr, true);  // per-launch
-  DevBuf<double> part((size_t)P * SL, s);
-  a.part = part.p;
+  DevBuf<double> own;
+  a.part = part_for(own, P);
   if (BT == 128) launch_rows_g<1, 128>(G, a, P, smem, s);
   else if (KB == 1) launch_rows_g<1, 256>(G, a, P, smem, s);
   else launch_rows_g<3, 256>(G, a, P, smem, s);
   SB_CHECK_LAUNCH(ctx);
-  reduce_rows_stats(ctx, part.p, P, R, stats, fuse);
+  reduce(a.part, P);
+}
+
+size_t rows_partials_cap(splatt_ctx* ctx, int R) {
+  return (size_t)4 * ctx->num_sms * stats_len(R);  // every path's P <= 4 x SMs
 }
 
 void lambda_gram(splatt_ctx* ctx, const double* stats, int R, bool first, double* lambda,

@@ -48,10 +48,23 @@ struct LambdaOut {
 // (stats_len(R)).  If !solve, M is ignored and A is only read.  Skipped when *status != 0.
 // tau: R column scales of M (from hadamard_inverse; used for <M, A>), NULL when !solve.
 // fuse: if non-NULL the reduction kernel also performs lambda_gram (single-rank path).
+// rr: run the reduction (and the fused lambda step) on rr->stream after an event recorded
+// behind the solve, from the persistent partial buffer rr->part (cap doubles, at least
+// rows_partials_cap), so the next MTTKRP on the context stream does not wait for it.  The
+// caller orders later users of `stats` / the fused outputs and of rr->part after rr->stream.
+struct RowsReduce {
+  cudaStream_t stream;
+  cudaEvent_t ev;
+  double* part;
+  size_t cap;
+  EventTimer* tm;  // optional span on rr->stream
+  int cat;
+};
 void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, uint64_t hi,
                       int R, int ld, const double* Vinv, const double* tau, bool solve,
                       bool inner, const int* status, double* stats,
-                      const LambdaOut* fuse = nullptr);
+                      const LambdaOut* fuse = nullptr, const RowsReduce* rr = nullptr);
+size_t rows_partials_cap(splatt_ctx* ctx, int R);
 
 // a8 + a9: lambda (first: 2-norm = sqrt(G~_rr); else max(1, colmax)), G_n =
 // G~ / (lambda lambda^T) (mirrored), inner_out = stats inner, sig = 1 / lambda (the
