@@ -34,6 +34,7 @@ double mttkrp_alg_bytes(const DevCsf& c, int R, int level = 0);
 // distinct[m] = rows of mode m the tensor references (or an upper bound).
 double mttkrp_min_bytes(const DevCsf& c, int R, int level, const uint64_t* distinct);
 
-int mttkrp_chunk_leaves(int N, int ld);
+// Leaves per ROOT/INTERNAL/LEAF work unit of tree `c` (its chunk table's granularity).
+int mttkrp_chunk_leaves(const DevCsf& c);
 
 }  // namespace sb

@@ -82,6 +82,10 @@ def test_chunk_boundaries(sb, ctx, nnz):
         for R in (8, 35):
             mttkrp_all(sb, ctx, t, R, "all", seed=R)
         mttkrp_all(sb, ctx, t, 16, "one", seed=1)
+    # long fibers (>= 4 leaves per fiber: the 512-leaf chunks of 3-mode trees)
+    t = synth.generate((4, 3, 5000), nnz, [("uniform",)] * 3, "u01", seed=nnz)
+    assert t.nnz == nnz
+    mttkrp_all(sb, ctx, t, 35, "all", seed=2)
 
 
 @pytest.mark.parametrize("policy", ["all", "one", "two"])
