@@ -183,6 +183,71 @@ __global__ void __launch_bounds__(256, 3) gather_ldg_w(const double* __restrict_
   }
 }
 
+
+// ---------------------------------------------------------------- A'': leaf records via smem or SHFL
+// 9-lane groups, 3 per warp, one 32-leaf chunk per group.  MODE 0: per-leaf id/value read
+// back from a per-group shared table (LDS.32 + LDS.64 broadcast); MODE 1: the group's lanes
+// hold ids/values in registers (lane gl holds leaves gl + 9 e) and each leaf's pair is
+// shuffled from its owner (warp-uniform register choice).
+template <int MODE>
+__global__ void __launch_bounds__(256, 3) gather_rec(const double* __restrict__ F,
+                                                     const uint32_t* __restrict__ idx,
+                                                     const double* __restrict__ val,
+                                                     uint64_t nchunks, double* __restrict__ out) {
+  __shared__ uint32_t sid[8][3][36];
+  __shared__ double sv[8][3][36];
+  const int lane = threadIdx.x & 31, g = lane / 9, gl = lane % 9, w = threadIdx.x >> 5;
+  const bool live = lane < 27;
+  const int gs = live ? g : 0;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+  for (uint64_t c0 = warp * 3; c0 < nchunks; c0 += nwarps * 3) {
+    const uint64_t c = c0 + gs;
+    const bool ok = live && c < nchunks;
+    uint32_t rid[4];
+    double rv[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = gl + 9 * e;
+      const bool in = ok && j < 32;
+      rid[e] = in ? __ldg(idx + c * 32 + j) : 0u;
+      rv[e] = in ? __ldg(val + c * 32 + j) : 0.0;
+      if (MODE == 0 && in) { sid[w][gs][j] = rid[e]; sv[w][gs][j] = rv[e]; }
+    }
+    __syncwarp();
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll 1
+    for (int j0 = 0; j0 < 32; j0 += 2) {
+      double4 r[2];
+      double v[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int j = j0 + u;
+        uint32_t id;
+        if (MODE == 0) {
+          id = sid[w][gs][j];
+          v[u] = sv[w][gs][j];
+        } else {
+          const int src = gs * 9 + (j % 9), e = j / 9;  // e warp-uniform
+          uint32_t x = e == 0 ? rid[0] : e == 1 ? rid[1] : e == 2 ? rid[2] : rid[3];
+          double y = e == 0 ? rv[0] : e == 1 ? rv[1] : e == 2 ? rv[2] : rv[3];
+          id = __shfl_sync(0xffffffffu, x, src);
+          v[u] = __shfl_sync(0xffffffffu, y, src);
+        }
+        const double* p = F + (size_t)id * LD + gl * 4;
+        asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                     : "=d"(r[u].x), "=d"(r[u].y), "=d"(r[u].z), "=d"(r[u].w) : "l"(p));
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        a0 += v[u] * r[u].x; a1 += v[u] * r[u].y; a2 += v[u] * r[u].z; a3 += v[u] * r[u].w;
+      }
+    }
+    if (ok) *reinterpret_cast<double4*>(out + c * LD + gl * 4) = make_double4(a0, a1, a2, a3);
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------- B: TMA gather4
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -385,6 +450,13 @@ int main(int argc, char** argv) {
            name, (unsigned long)I, (unsigned long)(nch * 32), zipf, ms, nch * 32 / (ms * 1e-3),
            nch * 32 * (double)ROWB / (ms * 1e-3) / 1e12, maxerr);
   };
+  if (getenv("RECS")) {
+    const int blocks = 3;
+    timeit([&] { gather_ldg<2, 36, 1><<<nsm * blocks, 256>>>(F, ix, v, nch, o1); }, "ldg U=2 global ids", o1);
+    timeit([&] { gather_rec<0><<<nsm * blocks, 256>>>(F, ix, v, nch, o1); }, "records in smem", o1);
+    timeit([&] { gather_rec<1><<<nsm * blocks, 256>>>(F, ix, v, nch, o1); }, "records via shfl", o1);
+    return 0;
+  }
   if (getenv("WIDTHS")) {
     // row-gather ceiling by row width (ld = 16 / 36 / 64 doubles), L1-allocating, U = 4
     for (int w : {16, 36, 64}) {
