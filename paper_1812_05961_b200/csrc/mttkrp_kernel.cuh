@@ -68,6 +68,9 @@ struct Args {
   uint32_t* headrow;
   uint32_t* tailrow;
   const int* conv;            // ALS converged (splatt_ctx::d_conv): nothing to do
+  // D = 0: chunk counter for dynamic assignment (zeroed before the launch; a persistent grid
+  // of groups takes chunks in order as they finish), nullptr = one chunk per group.
+  unsigned* work;
 };
 
 struct d4 { double x, y, z, w; };
@@ -282,7 +285,15 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
     }
   };
 
-  for (uint32_t c = group; c < a.nchunks; c += ngroups) {
+  // Next chunk of this group: dynamic (D = 0 with a counter: lane 0 of the group takes it,
+  // the group shares it) or static round-robin.
+  auto next_chunk = [&](uint32_t prev, bool first) -> uint32_t {
+    if (a.work == nullptr) return first ? group : prev + ngroups;
+    uint32_t v = 0;
+    if (q == 0) v = atomicAdd(a.work, 1u);
+    return __shfl_sync(gmask, v, gw * G);
+  };
+  for (uint32_t c = next_chunk(0, true); c < a.nchunks; c = next_chunk(c, false)) {
     const uint32_t k0 = c * a.chunk;
     const uint32_t k1 = min(k0 + a.chunk, a.nnz);
     uint32_t base[N - 1];
@@ -570,6 +581,24 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
   }();
   (void)attr;
   uint64_t blocks = ceil_div(c.nchunks, groups_per_block);
+  static const bool dyn_env = [] {
+    const char* e = getenv("SPLATT_DYN");
+    return !(e && *e == '0');
+  }();
+  if (D == 0 && dyn_env && blocks > (uint64_t)ctx->num_sms) {
+    // dynamic chunk assignment over a persistent grid: no partial last wave, and a group
+    // that drew cheap chunks takes more
+    int occ = 0;
+    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ, mttkrp_csf_kernel<N, D, G, U, MINB, L1A>, threads, smem));
+    occ = std::max(occ, 1);
+    if (blocks > (uint64_t)ctx->num_sms * occ) {
+      blocks = (uint64_t)ctx->num_sms * occ;
+      if (c.work.n < 1) c.work.alloc(1, ctx->stream);
+      SB_CUDA(cudaMemsetAsync(c.work.p, 0, sizeof(unsigned), ctx->stream));
+      a.work = c.work.p;
+    }
+  }
   if (D > 0) {
     // persistent grid: each group walks many chunks, so the privatised hot rows are
     // flushed once per group rather than once per chunk
