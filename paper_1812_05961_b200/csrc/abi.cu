@@ -42,7 +42,17 @@ template <typename F>
 splatt_status guard(splatt_ctx* ctx, F&& f) {
   try {
     if (ctx) ctx->err.clear();
+    // A non-sticky error left by an earlier runtime call outside the library (or an ignored
+    // status) must not be reported by this call's first launch check.
+    const cudaError_t pending = cudaGetLastError();
+    if (pending != cudaSuccess && getenv("SPLATT_DEBUG_ERRORS"))
+      fprintf(stderr, "[splatt] pending CUDA error at call entry: %s\n", cudaGetErrorString(pending));
     f();
+    if (getenv("SPLATT_DEBUG_ERRORS")) {
+      const cudaError_t left = cudaGetLastError();
+      if (left != cudaSuccess)
+        fprintf(stderr, "[splatt] CUDA error left by the call: %s\n", cudaGetErrorString(left));
+    }
     return SPLATT_OK;
   } catch (const Error& e) {
     if (ctx) ctx->err = e.what(); else g_noctx_err = e.what();

@@ -598,7 +598,7 @@ void tile_tree(splatt_ctx* ctx, DevCsf& c, int T) {
     SB_CUDA(cub::DeviceScan::InclusiveSum(temp.p, tb, par.p, par.p, (int)F, st));
     gather_minus1_kernel<<<grid, 256, 0, st>>>(par.p, node.p, nnz, tmp.p);  // parent + 1
     SB_CHECK_LAUNCH(ctx);
-    std::swap(node.p, tmp.p);
+    std::swap(node, tmp);  // whole buffers: one may be arena memory, the other pooled
   }
   // 2. stable order by tile (the tree order inside each tile is kept)
   DevBuf<uint32_t> key(nnz, st), key2(nnz, st), pos(nnz, st), perm(nnz, st);

@@ -205,7 +205,7 @@ struct DevBuf {
     }
   }
   void release() {
-    if (p && pooled) cudaFreeAsync(p, s);
+    if (p && pooled && cudaFreeAsync(p, s) != cudaSuccess) cudaGetLastError();  // no stale error
     p = nullptr;
     n = 0;
     pooled = false;

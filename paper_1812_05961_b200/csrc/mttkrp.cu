@@ -26,20 +26,24 @@ void mttkrp_launch_n3(splatt_ctx* ctx, DevCsf& c, int D, const double* const* f,
   }
 }
 
-// Leaves per work unit (measured on B200: c2/c4 best at 256 for N = 3, c5 at 1024 for N = 4
-// (+1.8% over 512, 2048 +1.3%; profiles/ab_r01/sweep17.txt); shorter chunks balance better,
-// longer ones amortise the per-chunk setup and seam rows).
+// Leaves per work unit (measured on B200 with dynamic chunk assignment: N = 3 best at 384
+// (c2 +3.8% over 256; 320 and 448+ worse, profiles/ab_r01/chunks_dyn.txt), N = 4 at 1024
+// (+1.8% over 512, 1536 -6%); shorter chunks balance better, longer ones amortise the
+// per-chunk setup and seam rows).
 #ifndef SB_MTTKRP_CHUNK3
-#define SB_MTTKRP_CHUNK3 256
+#define SB_MTTKRP_CHUNK3 384
+#endif
+#ifndef SB_MTTKRP_CHUNK3_LONG
+#define SB_MTTKRP_CHUNK3_LONG 512
 #endif
 #ifndef SB_MTTKRP_CHUNK
 #define SB_MTTKRP_CHUNK 1024
 #endif
 
 // N = 3: trees with long fibers (>= 4 leaves per level-(N-2) node on average, e.g. c3's
-// modes 1/2 at ~8) take chunks of twice the length: the per-chunk setup and seam rows are
-// amortised over more leaves while the fiber rows already are (c3 +7.8%, c2 -14% if applied
-// to its ~2.9-leaf fibers, c4 +0.5%; profiles/ab_r01/sweep18.txt).  SPLATT_CHUNK overrides.
+// modes 1/2 at ~8) take longer chunks (512): the per-chunk setup and seam rows are amortised
+// over more leaves (c3 +7.8% with static scheduling; c2's ~2.9-leaf fibers lose 12% at 512;
+// profiles/ab_r01/sweep18.txt, chunks_dyn.txt).  SPLATT_CHUNK overrides.
 #ifndef SB_MTTKRP_LONG_FIBER
 #define SB_MTTKRP_LONG_FIBER 4
 #endif
@@ -50,7 +54,7 @@ int mttkrp_chunk_leaves(const DevCsf& c) {
   }
   if (c.N != 3) return SB_MTTKRP_CHUNK;
   const uint64_t fibers = std::max<uint64_t>(1, c.nodes[c.N - 2]);
-  return c.nnz >= (uint64_t)SB_MTTKRP_LONG_FIBER * fibers ? 2 * SB_MTTKRP_CHUNK3 : SB_MTTKRP_CHUNK3;
+  return c.nnz >= (uint64_t)SB_MTTKRP_LONG_FIBER * fibers ? SB_MTTKRP_CHUNK3_LONG : SB_MTTKRP_CHUNK3;
 }
 
 double mttkrp_alg_bytes(const DevCsf& c, int R, int level) {

@@ -68,8 +68,9 @@ struct Args {
   uint32_t* headrow;
   uint32_t* tailrow;
   const int* conv;            // ALS converged (splatt_ctx::d_conv): nothing to do
-  // D = 0: chunk counter for dynamic assignment (zeroed before the launch; a persistent grid
-  // of groups takes chunks in order as they finish), nullptr = one chunk per group.
+  // Chunk counter for dynamic assignment (zeroed before the launch; a persistent grid of
+  // groups takes chunks in order as they finish), nullptr = static (one chunk per group for
+  // D = 0, round-robin over a persistent grid for D > 0).
   unsigned* work;
 };
 
@@ -285,8 +286,8 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
     }
   };
 
-  // Next chunk of this group: dynamic (D = 0 with a counter: lane 0 of the group takes it,
-  // the group shares it) or static round-robin.
+  // Next chunk of this group: dynamic (with a counter: lane 0 of the group takes it, the
+  // group shares it) or static round-robin.
   auto next_chunk = [&](uint32_t prev, bool first) -> uint32_t {
     if (a.work == nullptr) return first ? group : prev + ngroups;
     uint32_t v = 0;
@@ -608,6 +609,11 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
     occ = std::max(occ, 1);
     blocks = std::min<uint64_t>(blocks, (uint64_t)ctx->num_sms * occ);
     for (int h = 0; h < kHotRows; ++h) a.hot[h] = c.hot[D][h];
+    if (dyn_env) {  // chunks taken dynamically here too (the grid is persistent anyway)
+      if (c.work.n < 1) c.work.alloc(1, ctx->stream);
+      SB_CUDA(cudaMemsetAsync(c.work.p, 0, sizeof(unsigned), ctx->stream));
+      a.work = c.work.p;
+    }
   }
   mttkrp_csf_kernel<N, D, G, U, MINB, L1A>
       <<<(unsigned)std::max<uint64_t>(1, blocks), threads, smem, ctx->stream>>>(a);
