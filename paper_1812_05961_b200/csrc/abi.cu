@@ -287,6 +287,8 @@ splatt_status splatt_csf_build(splatt_ctx* ctx, const splatt_coo* coo, int32_t n
     }
     build_csf_set(ctx, X.view.ind, X.view.vals, X.view.nnz, nmodes, X.view.dims, roots, c->ncsf,
                   outs);
+    for (int m = 0; m < nmodes; ++m)
+      if (c->mode_level[m] > 0) c->csf[c->mode_csf[m]]->nonroot = true;
     *out = c.release();
   });
 }

@@ -269,6 +269,8 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       csf[k] = owned[k].get();
     }
     build_csf_set(ctx, X.ind, X.vals, X.nnz, N, X.dims, roots, ncsf, csf.data());
+    for (int n = 0; n < N; ++n)
+      if (mode_level[n] > 0) csf[mode_csf[n]]->nonroot = true;
     if (late_norm) {
       wait_vals(ctx);  // (the build's decode already did)
       norm_sq(ctx, X.vals, X.nnz, normx.p);

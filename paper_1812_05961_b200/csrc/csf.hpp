@@ -40,6 +40,9 @@ struct DevCsf {
   // L1-allocating.  cpd_als times both on its first two iterations and keeps the faster
   // (DESIGN.md §4.2); the choice changes no arithmetic.
   int l1a = -1;
+  // Some mode runs an INTERNAL/LEAF traversal over this tree (policies ONE/TWO): its chunk
+  // table uses the non-root kernels' best chunk length (mttkrp_chunk_leaves).
+  bool nonroot = false;
   bool hot_ready[SPLATT_MAX_NMODES] = {false};
   // Leaf-mode tiling for the ROOT MTTKRP: when the leaf factor does
   // not fit in L2, the same tree split by leaf-id range into tiles (each a tree with the same
