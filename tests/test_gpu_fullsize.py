@@ -109,6 +109,25 @@ def test_c2_full(sb, ctx):
     als_check(sb, ctx, t, c["rank"], c["iters"], c["seed"])
 
 
+@pytest.mark.parametrize("policy", ["one", "two"])
+def test_c2_full_policies(sb, ctx, policy):
+    """c2 under the ONE / TWO allocation policies, as `bench.py --policy` runs it: INTERNAL and
+    LEAF traversals (bulk row reductions, hot rows, dynamic chunks over a persistent grid,
+    256-leaf chunks on the shared tree) for 20 iterations against the oracle."""
+    t = tensor("c2")
+    c = synth.config("c2")
+    ind, vals = dev_coo(t)
+    res = sb.cpd_als(ind, vals, t.dims, rank=c["rank"], max_iters=c["iters"], tol=0.0,
+                     seed=c["seed"], ctx=ctx, policy=policy)
+    ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=c["rank"], max_iters=c["iters"], tol=0.0,
+                         seed=c["seed"])
+    for n in range(t.nmodes):
+        e = rel_fro(res["factors"][n].cpu().numpy(), ref["factors"][n])
+        assert e <= ALS_TOL, (n, e)
+    assert rel_fro(res["lam"].cpu().numpy(), ref["lam"]) <= ALS_TOL
+    assert abs(res["fit"] - ref["fit"]) <= ALS_TOL * abs(ref["fit"])
+
+
 @pytest.mark.parametrize("name", ["c3", "c4", "c4r64", "c5"])
 def test_large_configs(sb, ctx, name):
     t = tensor(name.replace("r64", "") if name == "c4r64" else name)
