@@ -371,6 +371,26 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   }
   for (int n = 0; n < N; ++n)  // chunk tables / hot ids before the loop (no syncs inside it)
     mttkrp_prepare(ctx, *csf[sharded ? n : mode_csf[n]], sharded ? 0 : mode_level[n], ld);
+  // The loop's MTTKRPs share each tree's chunk counter, zeroed once here (DevCsf::work_seq);
+  // the sequence ends with the call, also on an error.
+  struct WorkSeq {
+    std::vector<DevCsf*> trees;
+    ~WorkSeq() { for (DevCsf* t : trees) { t->work_seq = false; } }
+  } work_seq;
+  for (int k = 0; k < (sharded ? N : ncsf); ++k) {
+    DevCsf* c = csf[k];
+    if (!c || !c->nnz) continue;
+    std::vector<DevCsf*> ts{c};
+    for (auto& t : c->tiles) ts.push_back(t.get());
+    for (DevCsf* t : ts) {
+      ArenaScope own(t->arena, false);
+      if (t->work.n < 1) t->work.alloc(1, s);
+      SB_CUDA(cudaMemsetAsync(t->work.p, 0, sizeof(unsigned), s));
+      t->work_base = 0;
+      t->work_seq = true;
+      work_seq.trees.push_back(t);
+    }
+  }
   tm.end();
   tr.mark("csf builds");
 

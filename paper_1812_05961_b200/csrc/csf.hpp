@@ -31,7 +31,9 @@ struct DevCsf {
   DevBuf<double> seam;  // MTTKRP scratch: one row per chunk (chunk-seam slices)
   DevBuf<double> tail;  // deterministic mode: the open slice's row at each chunk end
   DevBuf<uint32_t> seamrows;  // deterministic mode: head / tail output rows per chunk
-  DevBuf<unsigned> work;      // ROOT MTTKRP: dynamic chunk counter
+  DevBuf<unsigned> work;      // MTTKRP: dynamic chunk counter
+  unsigned work_base = 0;     // its value at the next launch's start
+  bool work_seq = false;      // inside a launch sequence (cpd_als): no per-launch zeroing
   uint64_t dims[SPLATT_MAX_NMODES] = {0};  // length of the mode at each level
   // Non-root MTTKRP: the kHotRows (8) most frequent ids of each level (~0u = unused), computed on
   // first use of that level as an output level.

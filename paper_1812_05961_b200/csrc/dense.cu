@@ -432,8 +432,12 @@ struct MmaShape {
   static constexpr int NP = NT * (NT + 1) / 2;  // upper-triangular 8x8 Gram tiles
 };
 
+#ifndef SB_MMA_MINB
+#define SB_MMA_MINB 1
+#endif
+constexpr int mma_minb(int NT) { return NT <= 5 ? SB_MMA_MINB : 1; }
 template <int NT, int W>
-__global__ void __launch_bounds__(W * 32, 1) solve_gram_mma_kernel(const RowsArgs a) {
+__global__ void __launch_bounds__(W * 32, mma_minb(NT)) solve_gram_mma_kernel(const RowsArgs a) {
   using Sh = MmaShape<NT>;
   constexpr int RP = Sh::RP, LDP = Sh::LDP, NP = Sh::NP;
   constexpr int KS = RP / 4;  // k-steps upper bound (ld <= RP)
@@ -956,7 +960,7 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
     const uint64_t nslabs = ceil_div(hi - lo, 8);
     a.ntiles = nslabs;
     const int Pm = (int)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(nslabs, W),
-                                                                 (uint64_t)ctx->num_sms));
+                                                                 (uint64_t)ctx->num_sms * mma_minb(NT)));
     ArenaScope scratch(current_arena() ? ctx->arena_scratch : nullptr, true);  // per-launch
     DevBuf<double> own;
     a.part = part_for(own, Pm);

@@ -72,6 +72,10 @@ struct Args {
   // groups takes chunks in order as they finish), nullptr = static (one chunk per group for
   // D = 0, round-robin over a persistent grid for D > 0).
   unsigned* work;
+  // Counter value at launch start: a launch takes exactly nchunks + ngroups values (every
+  // group's last take overshoots once), so a sequence of launches can share one counter
+  // zeroed once (DevCsf::work_seq) instead of a memset per launch.
+  unsigned work_base;
 };
 
 struct d4 { double x, y, z, w; };
@@ -291,7 +295,7 @@ __global__ void __launch_bounds__(kBlock, MINB) mttkrp_csf_kernel(const Args<N> 
   auto next_chunk = [&](uint32_t prev, bool first) -> uint32_t {
     if (a.work == nullptr) return first ? group : prev + ngroups;
     uint32_t v = 0;
-    if (q == 0) v = atomicAdd(a.work, 1u);
+    if (q == 0) v = atomicAdd(a.work, 1u) - a.work_base;
     return __shfl_sync(gmask, v, gw * G);
   };
   for (uint32_t c = next_chunk(0, true); c < a.nchunks; c = next_chunk(c, false)) {
@@ -557,6 +561,23 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
   a.R = R;
   a.accumulate = acc & 1;
   a.conv = ctx->d_conv;
+  // The tree's chunk counter for this launch (alloc'd from the tree's allocator): inside a
+  // sequence (DevCsf::work_seq, set by cpd_als after zeroing it once) the launch starts at
+  // the running base, else the counter is zeroed first.
+  auto take_counter = [&](uint64_t ngroups) -> unsigned* {
+    if (c.work.n < 1) {
+      c.work.alloc(1, ctx->stream);
+      SB_CUDA(cudaMemsetAsync(c.work.p, 0, sizeof(unsigned), ctx->stream));
+      c.work_base = 0;
+    }
+    if (!c.work_seq) {
+      SB_CUDA(cudaMemsetAsync(c.work.p, 0, sizeof(unsigned), ctx->stream));
+      c.work_base = 0;
+    }
+    a.work_base = c.work_base;
+    c.work_base += (unsigned)(c.nchunks + ngroups);
+    return c.work.p;
+  };
   if (D == 0 && ctx->deterministic) {
     if (c.tail.n < c.nchunks * (size_t)ld) c.tail.alloc(c.nchunks * (size_t)ld, ctx->stream);
     if (c.seamrows.n < 2 * c.nchunks) c.seamrows.alloc(2 * c.nchunks, ctx->stream);
@@ -595,9 +616,7 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
     occ = std::max(occ, 1);
     if (blocks > (uint64_t)ctx->num_sms * occ) {
       blocks = (uint64_t)ctx->num_sms * occ;
-      if (c.work.n < 1) c.work.alloc(1, ctx->stream);
-      SB_CUDA(cudaMemsetAsync(c.work.p, 0, sizeof(unsigned), ctx->stream));
-      a.work = c.work.p;
+      a.work = take_counter(blocks * groups_per_block);
     }
   }
   if (D > 0) {
@@ -609,11 +628,8 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
     occ = std::max(occ, 1);
     blocks = std::min<uint64_t>(blocks, (uint64_t)ctx->num_sms * occ);
     for (int h = 0; h < kHotRows; ++h) a.hot[h] = c.hot[D][h];
-    if (dyn_env) {  // chunks taken dynamically here too (the grid is persistent anyway)
-      if (c.work.n < 1) c.work.alloc(1, ctx->stream);
-      SB_CUDA(cudaMemsetAsync(c.work.p, 0, sizeof(unsigned), ctx->stream));
-      a.work = c.work.p;
-    }
+    if (dyn_env)  // chunks taken dynamically here too (the grid is persistent anyway)
+      a.work = take_counter(blocks * groups_per_block);
   }
   mttkrp_csf_kernel<N, D, G, U, MINB, L1A>
       <<<(unsigned)std::max<uint64_t>(1, blocks), threads, smem, ctx->stream>>>(a);
