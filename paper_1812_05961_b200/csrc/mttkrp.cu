@@ -124,13 +124,35 @@ void ensure_hot(splatt_ctx* ctx, DevCsf& c, int level) {
   c.hot_ready[level] = true;
 }
 
-// Deterministic chunk seams: every chunk whose first slice closed in it (head) sums, in
-// chunk order, the tails of the chunks the slice spans and its own head row into the output
-// row (the only writer of that row).  One warp per chunk, lanes over columns.
+// Deterministic chunk seams: every chunk whose first slice closed in it (head) sums, in a
+// fixed order, the tails of the chunks the slice spans and its own head row into the output
+// row (the only writer of that row).  One warp per chunk, lanes over columns; the span start
+// is found 32 chunks per step (ballot).  Spans longer than kLongSpan chunks (a power-law
+// slice can cover thousands) are queued for seam_long_kernel, which splits them over a
+// block.  The summation order is a function of the span alone (4 interleaved partial sums
+// per lane; 8 contiguous warp ranges for long spans), so the result is bitwise reproducible.
+constexpr int kLongSpan = 64;
+static_assert(kLongSpan >= mk::kLongSpanMin, "long-span list sized for kLongSpanMin");
+
+__device__ __forceinline__ double sum_tails(const double* __restrict__ tail, uint64_t k0,
+                                            uint64_t k1, int ld, int col) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  uint64_t k = k0;
+  for (; k + 4 <= k1; k += 4) {
+    a0 += tail[k * ld + col];
+    a1 += tail[(k + 1) * ld + col];
+    a2 += tail[(k + 2) * ld + col];
+    a3 += tail[(k + 3) * ld + col];
+  }
+  for (; k < k1; ++k) a0 += tail[k * ld + col];
+  return (a0 + a1) + (a2 + a3);
+}
+
 __global__ void seam_combine_kernel(const double* __restrict__ head, const double* __restrict__ tail,
                                     const uint32_t* __restrict__ headrow,
                                     const uint32_t* __restrict__ tailrow, uint64_t nchunks, int ld,
-                                    double* __restrict__ out, int accumulate, const int* conv) {
+                                    double* __restrict__ out, int accumulate, const int* conv,
+                                    uint32_t* __restrict__ longcnt, uint64_t* __restrict__ longlist) {
   if (conv && *conv) return;
   const uint64_t c = blockIdx.x * (uint64_t)(blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
@@ -138,13 +160,56 @@ __global__ void seam_combine_kernel(const double* __restrict__ head, const doubl
   const uint32_t s = headrow[c];
   if (s == ~0u) return;
   uint64_t c0 = c;
-  while (c0 > 0 && tailrow[c0 - 1] == s) --c0;
+  for (;;) {  // chunks c0-1, c0-2, ... whose open tail is slice s
+    const int64_t k = (int64_t)c0 - 1 - lane;
+    const unsigned m = __ballot_sync(0xffffffffu, k >= 0 && tailrow[k] == s);
+    if (m == 0xffffffffu) { c0 -= 32; continue; }
+    c0 -= (uint64_t)(__ffs(~m) - 1);
+    break;
+  }
+  if (c - c0 > (uint64_t)kLongSpan) {
+    if (lane == 0) {
+      const uint32_t e = atomicAdd(longcnt, 1u);
+      longlist[2 * (uint64_t)e] = c;
+      longlist[2 * (uint64_t)e + 1] = c0;
+    }
+    return;
+  }
   for (int col = lane; col < ld; col += 32) {
-    double acc = 0.0;
-    for (uint64_t k = c0; k < c; ++k) acc += tail[k * ld + col];
-    acc += head[c * ld + col];
+    const double acc = sum_tails(tail, c0, c, ld, col) + head[c * ld + col];
     double* o = out + (size_t)s * ld + col;
     *o = accumulate ? *o + acc : acc;
+  }
+}
+
+// Long spans: one block (8 warps) per span, warp w sums the w-th of 8 contiguous ranges,
+// the partials are added in warp order.
+__global__ void __launch_bounds__(256) seam_long_kernel(
+    const double* __restrict__ head, const double* __restrict__ tail,
+    const uint32_t* __restrict__ headrow, int ld, double* __restrict__ out, int accumulate,
+    const int* conv, const uint32_t* __restrict__ longcnt,
+    const uint64_t* __restrict__ longlist) {
+  if (conv && *conv) return;
+  __shared__ double part[8][SPLATT_MAX_RANK];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t n = *longcnt;
+  for (uint32_t e = blockIdx.x; e < n; e += gridDim.x) {
+    const uint64_t c = longlist[2 * (uint64_t)e], c0 = longlist[2 * (uint64_t)e + 1];
+    const uint64_t span = c - c0;
+    const uint64_t k0 = c0 + span * w / 8, k1 = c0 + span * (w + 1) / 8;
+    for (int col = lane; col < ld; col += 32) part[w][col] = sum_tails(tail, k0, k1, ld, col);
+    __syncthreads();
+    if (w == 0) {
+      const uint32_t s = headrow[c];
+      for (int col = lane; col < ld; col += 32) {
+        double acc = 0.0;
+        for (int v = 0; v < 8; ++v) acc += part[v][col];
+        acc += head[c * ld + col];
+        double* o = out + (size_t)s * ld + col;
+        *o = accumulate ? *o + acc : acc;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -201,10 +266,18 @@ void mttkrp_level(splatt_ctx* ctx, DevCsf& c, int level, const double* const* fa
       default: mttkrp_launch_nx(ctx, t, level, fac_by_mode, out, ld, R, chunk, accumulate); break;
     }
     if (level == 0 && ctx->deterministic) {
+      // seamrows: head rows | tail rows | long-span count | (pad) | long-span (c, c0) pairs
+      uint32_t* longcnt = t.seamrows.p + 2 * t.nchunks;
+      uint64_t* longlist = reinterpret_cast<uint64_t*>(t.seamrows.p + 2 * t.nchunks + 2);
+      SB_CUDA(cudaMemsetAsync(longcnt, 0, sizeof(uint32_t), ctx->stream));
       const unsigned blocks = (unsigned)ceil_div(t.nchunks, 8);
       seam_combine_kernel<<<std::max(1u, blocks), 256, 0, ctx->stream>>>(
           t.seam.p, t.tail.p, t.seamrows.p, t.seamrows.p + t.nchunks, t.nchunks, ld, out,
-          accumulate & 1, ctx->d_conv);
+          accumulate & 1, ctx->d_conv, longcnt, longlist);
+      SB_CHECK_LAUNCH(ctx);
+      seam_long_kernel<<<(unsigned)ctx->num_sms, 256, 0, ctx->stream>>>(
+          t.seam.p, t.tail.p, t.seamrows.p, ld, out, accumulate & 1, ctx->d_conv, longcnt,
+          longlist);
       SB_CHECK_LAUNCH(ctx);
     }
   };

@@ -185,6 +185,9 @@ struct MetaLayout {
 };
 
 constexpr int kBatch = 32;
+// Deterministic seams: a long-span entry needs > kLongSpanMin chunks, so at most
+// nchunks / kLongSpanMin of them exist (mttkrp.cu's kLongSpan must not be smaller).
+constexpr int kLongSpanMin = 64;
 constexpr int kBlock = 256;
 
 // Per-group table: records + values, plus 4 words of padding so that the tables of the
@@ -580,7 +583,9 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
   };
   if (D == 0 && ctx->deterministic) {
     if (c.tail.n < c.nchunks * (size_t)ld) c.tail.alloc(c.nchunks * (size_t)ld, ctx->stream);
-    if (c.seamrows.n < 2 * c.nchunks) c.seamrows.alloc(2 * c.nchunks, ctx->stream);
+    // head rows, tail rows, long-span count (+1 pad word), (c, c0) pairs for long spans
+    const size_t words = 2 * c.nchunks + 2 + 4 * ((c.nchunks + kLongSpanMin - 1) / kLongSpanMin + 1);
+    if (c.seamrows.n < words) c.seamrows.alloc(words, ctx->stream);
     a.det = 1;
     a.tail = c.tail.p;
     a.headrow = c.seamrows.p;
