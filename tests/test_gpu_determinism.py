@@ -80,8 +80,8 @@ def test_deterministic_als_bitwise_repeatable(sb):
 
 
 def test_gather_policy_tuning_changes_no_bits(sb, monkeypatch):
-    """cpd_als times the ROOT gathers with L1::no_allocate (iteration 1) and L1-allocating
-    loads (iteration 2) per tree (>= 2^20 nonzeros) and keeps the faster: the choice must not
+    """cpd_als times the ROOT gathers with L1-allocating loads (iteration 2) and
+    L1::no_allocate (iteration 3) per tree (>= 2^20 nonzeros) and keeps the faster: the choice must not
     change a bit of the result (deterministic context), whichever way it goes."""
     t = synth.generate((40_000, 11_000, 75_000), 1_100_000, [("zipf", 1.1)] * 3, "ratings",
                        seed=23)
