@@ -311,6 +311,18 @@ def test_cpd_als_tol_stops_like_oracle(sb, ctx, tol):
     als_compare(res, ref)
 
 
+def test_cpd_als_host_input_with_tol(sb, ctx):
+    """Host-staged COO (values uploaded on the copy stream during the sort, ||X|| taken after
+    the build) with the device-side convergence test: same stopping iteration and model as
+    the oracle, host outputs."""
+    t = tensors()[0]
+    res = sb.cpd_als(t.ind, t.vals, t.dims, rank=8, max_iters=100, tol=1e-4, seed=1, ctx=ctx,
+                     out_device=False)
+    ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=8, max_iters=100, tol=1e-4, seed=1)
+    assert res["iters"] == ref["iters"] < 100
+    als_compare(res, ref)
+
+
 def test_errors(sb, ctx):
     t = synth.random_tiny(3)
     ind, vals = dev_coo(t)
