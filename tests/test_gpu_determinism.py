@@ -79,12 +79,13 @@ def test_deterministic_als_bitwise_repeatable(sb):
     als_compare(runs[0], ref)
 
 
-def test_gather_policy_tuning_changes_no_bits(sb, monkeypatch):
+@pytest.mark.parametrize("N", [3, 4])
+def test_gather_policy_tuning_changes_no_bits(sb, monkeypatch, N):
     """cpd_als times the ROOT gathers with L1-allocating loads (iteration 2) and
     L1::no_allocate (iteration 3) per tree (>= 2^20 nonzeros) and keeps the faster: the choice must not
     change a bit of the result (deterministic context), whichever way it goes."""
-    t = synth.generate((40_000, 11_000, 75_000), 1_100_000, [("zipf", 1.1)] * 3, "ratings",
-                       seed=23)
+    dims = (40_000, 11_000, 75_000) if N == 3 else (20_000, 5_000, 1_000, 50)
+    t = synth.generate(dims, 1_200_000, [("zipf", 1.1)] * N, "ratings", seed=23)
     ctx = sb.Context(0)
     ctx.set_deterministic(True)
     ind, vals = dev_coo(t)
@@ -94,10 +95,10 @@ def test_gather_policy_tuning_changes_no_bits(sb, monkeypatch):
             monkeypatch.delenv("SPLATT_L1_ALLOC", raising=False)
         else:
             monkeypatch.setenv("SPLATT_L1_ALLOC", force)
-        runs.append(sb.cpd_als(ind, vals, t.dims, rank=35, max_iters=5, seed=5, ctx=ctx,
+        runs.append(sb.cpd_als(ind, vals, t.dims, rank=35 if N == 3 else 16, max_iters=5, seed=5, ctx=ctx,
                                out_device=False, stats=True))
     for r in runs[1:]:
-        for n in range(3):
+        for n in range(N):
             assert np.array_equal(r["factors"][n].view(np.uint64),
                                   runs[0]["factors"][n].view(np.uint64))
         assert np.array_equal(r["lam"].view(np.uint64), runs[0]["lam"].view(np.uint64))
