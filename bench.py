@@ -7,10 +7,15 @@ mode, factor init, `iters` CP-ALS iterations (Hadamard+Cholesky, MTTKRP, solve,
 normalise, Gram refresh, fit), finalise.  value = (N_modes * nnz * R * iters) per
 second of step time, summed over all ranks' shared work (whole-job throughput).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl reference]
 
-N>1: launch under torchrun; the path is sharded by root slices with
-NCCL all-reduce / all-gather inside the library ("scaling": "strong", fixed tensor).
+Default workload: c5 (BASELINE.json configs[4]: 4-mode, 150M nonzeros, R=16, 20 iterations),
+the largest configuration the metric is stated on ("at 1/2/4/8 B200", BJ:2, :9, :11) that
+fits one GPU; c3 (the other one) and c2/c4 via --config.
+N>1: one process per GPU.  Under torchrun (WORLD_SIZE set) each rank runs directly;
+otherwise `bench.py --gpus N` re-executes itself under torch.distributed.run with N ranks
+on 127.0.0.1.  The path is sharded by root slices / equal nonzero ranges
+with NCCL all-reduce / all-gather inside the library ("scaling": "strong", fixed tensor).
 --impl reference times the CPU oracle (the tier's reference arm) on the host cores.
 """
 from __future__ import annotations
@@ -30,7 +35,7 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-DEFAULT_CONFIG = "c2"  # BASELINE.json configs[1] (YELP-shaped), the metric's N=1 workload
+DEFAULT_CONFIG = "c5"  # BASELINE.json configs[4]: the largest config the metric names at 1/2/4/8 GPUs
 METRIC = "MTTKRP nnz·R/s and CP-ALS s/iter (fp64), % HBM roofline"
 UNIT = "nnz·R/s"
 
@@ -188,28 +193,77 @@ def algorithmic_units(cfg):
     return N * cfg["nnz"] * cfg["rank"] * cfg["iters"]
 
 
-def cpu_baseline(t, cfg, iters=None):
-    """The oracle as it stands, on the host cores, on a bounded sample of the iterations."""
-    iters = iters or min(cfg["iters"], 10)
+# Oracle iterations per cpu_baseline sample (about 10-30 s of host work on 16 cores) and per
+# reference-arm step (one iteration: each step is a bounded sample of the same workload).
+CPU_SAMPLE_ITERS = {"c1": 10, "c2": 10, "c3": 2, "c4": 2, "c4r64": 2, "c5": 2}
+
+
+def host_cpu_info():
+    """lscpu model / sockets / cores (the oracle's cores are stated)."""
+    info = {"logical_cpus": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {}
+        for ln in out.splitlines():
+            if ":" in ln:
+                k, v = ln.split(":", 1)
+                kv[k.strip()] = v.strip()
+        info["model"] = kv.get("Model name")
+        for k, name in (("Socket(s)", "sockets"), ("Core(s) per socket", "cores_per_socket"),
+                        ("Thread(s) per core", "threads_per_core")):
+            if kv.get(k, "").isdigit():
+                info[name] = int(kv[k])
+    except Exception:
+        pass
+    info["omp_proc_bind"] = os.environ.get("OMP_PROC_BIND")
+    info["omp_num_threads"] = os.environ.get("OMP_NUM_THREADS")
+    return info
+
+
+def _oracle_run(t, cfg, iters):
     import oracle
     t0 = time.perf_counter()
     r = oracle.cpd_als(t.dims, t.ind, t.vals, rank=cfg["rank"], max_iters=iters, tol=0.0,
                        seed=cfg["seed"], timings=True)
     wall = time.perf_counter() - t0
     tm = r["timings"]
-    step = tm["loop"] + tm["sort"]
     units = len(t.dims) * t.nnz * cfg["rank"] * iters
-    return {"value": units / step, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{cfg['name']} full tensor, {iters} of {cfg['iters']} CP-ALS iterations "
-                      f"(+ its per-mode grouping sort); wall {wall:.1f}s",
-            "sec_per_iter": tm["loop"] / iters,
-            "mttkrp_nnzR_per_s": len(t.dims) * t.nnz * cfg["rank"] * iters / tm["mttkrp"]}
+    return units, tm, wall
+
+
+def cpu_baseline(t, cfg, iters=None):
+    """The oracle as it stands, on the host cores, on a bounded sample of the iterations,
+    plus a 1-thread leg on c1 (full run) mirroring the paper's 1-thread column."""
+    import oracle
+    import synth
+    iters = iters or CPU_SAMPLE_ITERS.get(cfg["name"], 2)
+    units, tm, wall = _oracle_run(t, cfg, iters)
+    step = tm["loop"] + tm["sort"]
+    out = {"value": units / step, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+           "sample": f"{cfg['name']} full tensor, {iters} of {cfg['iters']} CP-ALS iterations "
+                     f"(+ its per-mode grouping sort); wall {wall:.1f}s",
+           "sec_per_iter": tm["loop"] / iters,
+           "mttkrp_nnzR_per_s": units / tm["mttkrp"],
+           "host": host_cpu_info()}
+    nthr = oracle.num_threads()
+    try:
+        oracle.set_threads(1)
+        c1 = dict(synth.config("c1"), name="c1")
+        t1 = synth.generate_config("c1")
+        u1, tm1, _ = _oracle_run(t1, c1, c1["iters"])
+        out["one_thread"] = {"workload": "c1", "iters": c1["iters"],
+                             "value": u1 / (tm1["loop"] + tm1["sort"]), "unit": UNIT,
+                             "sec_per_iter": tm1["loop"] / c1["iters"]}
+    finally:
+        oracle.set_threads(nthr)
+    return out
 
 
 def run_reference(args, cfg, t):
     """--impl reference: the CPU oracle (this tier's reference arm), rank 0 only."""
     import oracle
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     iters = 1
@@ -229,13 +283,29 @@ def run_reference(args, cfg, t):
         "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_block(cfg, args.gpus),
+        "world_size": world,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(),
                          "kind": "oracle",
                          "sample": f"{cfg['name']} full tensor, {iters} CP-ALS iteration per step "
-                                   "(+ per-mode grouping sort)"},
+                                   "(+ per-mode grouping sort)",
+                         "host": host_cpu_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def self_launch(args):
+    """`bench.py --gpus N` outside torchrun: re-execute under torch.distributed.run with N ranks
+    (one process per GPU, rendezvous on 127.0.0.1).  Returns the launcher's exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    log(f"[bench] self-launch: {' '.join(cmd)}")
+    return subprocess.call(cmd)
 
 
 def config_block(cfg, G, policy="all", leaf_tiling="auto"):
@@ -269,6 +339,16 @@ def main():
                     help="multi-GPU split: per-mode auto, equal nonzero ranges (P2), whole slices (P1)")
     args = ap.parse_args()
 
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(self_launch(args))
+    if args.impl == "reference" and rank != 0:
+        return  # the reference arm runs on rank 0 only; the other ranks exit without work
+    # the oracle legs (reference arm, cpu_baseline) spread their OpenMP threads over the
+    # host's cores; libgomp reads this when the oracle library loads
+    os.environ.setdefault("OMP_PROC_BIND", "spread")
+
     import synth
     cfg = dict(synth.config(args.config))
     cfg["name"] = args.config
@@ -287,11 +367,12 @@ def main():
     import torch.distributed as dist
     import paper_1812_05961_b200 as sb
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"rank {rank}: LOCAL_RANK {local} but {torch.cuda.device_count()} "
+                         "visible GPUs")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
@@ -400,15 +481,18 @@ def main():
     launches = sum(s["mttkrp_launches"] for s in st)
     peak, peak_src = peaks()
     achieved = alg_bytes / t_mttkrp / 1e9 if t_mttkrp > 0 else 0.0
-    traffic = None
+    # DRAM bytes and L1TEX wavefront load per ROOT launch from the committed ncu capture of
+    # this config (profiles/mttkrp_traffic.json; ncu cannot run inside a timed bench)
+    traffic, ncu_rec = None, {}
     tf = os.path.join(ROOT, "profiles", "mttkrp_traffic.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf) and args.policy == "all":
         try:
             with open(tf) as f:
-                d = json.load(f).get(f"{args.config}:G{world}")
-            traffic = d and d.get("dram_bytes_per_launch")
+                ncu_rec = json.load(f).get(f"{args.config}:G{world}") or {}
+            traffic = ncu_rec.get("dram_bytes_per_launch")
         except Exception:
-            traffic = None
+            traffic, ncu_rec = None, {}
+    avg_launch_s = t_mttkrp / max(1, launches)
     units = algorithmic_units(cfg) * args.steps
     value = units / (ms * 1e-3)
     loop = [s["t_loop"] for s in st]
@@ -439,7 +523,22 @@ def main():
                      # ceiling of the gather primitive, profiles/gather_peak.json)
                      "gather": gather_view(st, N, R, t_mttkrp, args.policy),
                      "avg_launch_ms": 1e3 * t_mttkrp / max(1, launches),
-                     "launches": launches},
+                     "launches": launches,
+                     # three views of the same launches, side by side: algorithmic bytes
+                     # (every gather at HBM, the north star's roofline), the physical DRAM
+                     # bytes ncu measured, and the L1TEX data-pipe load that actually binds
+                     "views": {
+                         "alg_frac_of_hbm": achieved / peak,
+                         "dram_frac_of_hbm": (traffic / avg_launch_s / 1e9 / peak
+                                              if traffic and avg_launch_s > 0 else None),
+                         "dram_over_compulsory": (traffic / (min_bytes / max(1, launches))
+                                                  if traffic and min_bytes else None),
+                         "l2_hit_pct": ncu_rec.get("l2_hit_rate_pct"),
+                         "l1tex_wavefront_pct": ncu_rec.get("l1tex_wavefront_pct"),
+                         "ncu_source": ncu_rec.get("source"),
+                     }},
+        "comm": {"backend": "nccl" if world > 1 else None,
+                 "nranks": int(st[0].get("nranks", 1)) if st else None},
         "gpu_launches": sum(s["kernel_launches"] for s in st),
         "clocks": clk.summary() if clk else None,
         "e2e": e2e,

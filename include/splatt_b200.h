@@ -49,7 +49,7 @@ typedef enum {
   SPLATT_ERR_CUDA = -4,        /* CUDA runtime error (message in splatt_last_error)     */
   SPLATT_ERR_NCCL = -5,        /* NCCL error or NCCL library not loadable               */
   SPLATT_ERR_EMPTY = -6,       /* ||X|| = 0: the fit is undefined         */
-  SPLATT_ERR_UNSUPPORTED = -7  /* valid but outside this build (e.g. nnz >= 2^32)       */
+  SPLATT_ERR_UNSUPPORTED = -7  /* valid but outside this build (nnz >= 2^31)           */
 } splatt_status;
 
 enum { SPLATT_MAX_NMODES = 8, SPLATT_MAX_RANK = 128 };
@@ -99,7 +99,8 @@ typedef struct {
  * inverse and the fit run on a side stream overlapped with the MTTKRP: their spans
  * (including any wait for a free SM) are reported apart, in t_aux_*.                */
 typedef struct {
-  double   t_mttkrp;        /* all MTTKRP launches (incl. output zeroing)               */
+  double   t_mttkrp;        /* all MTTKRP kernel launches (the output zero-fill before */
+                            /*   a ROOT launch is excluded; it is not counted anywhere)  */
   double   t_build;         /* validation + COO->CSF build ("Sort")                     */
   double   t_ata;           /* Hadamard of Grams + Gram refresh ("Mat A^TA")           */
   double   t_norm;          /* partial reduction + lambda ("Mat norm"); one rank: on the  */
@@ -233,7 +234,7 @@ splatt_status splatt_ctx_set_leaf_tiling(splatt_ctx* ctx, double l2_fraction);
  * Bit-exact: the result is a pure integer function of the input.
  * nmodes and dims must equal coo->nmodes / coo->dims (they follow the north star's
  * call shape).  Errors: BADINPUT (nmodes, nnz = 0, dims, index >= dim, unknown
- * policy, mismatch), UNSUPPORTED (nnz >= 2^32).                                     */
+ * policy, mismatch), UNSUPPORTED (nnz >= 2^31: 32-bit leaf positions and sort counts). */
 splatt_status splatt_csf_build(splatt_ctx* ctx, const splatt_coo* coo, int32_t nmodes,
                                const uint64_t* dims, int32_t policy, splatt_csf** out);
 /* Allocation of a built CSF set: *ncsf (ALL: N, ONE: 1, TWO: 2) and, for mode `mode`,

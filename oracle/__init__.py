@@ -61,7 +61,6 @@ def lib():
             L.oracle_hadamard_except.argtypes = [i32, i32, P, i32, P]
             L.oracle_group_by_mode.argtypes = [u64, P, u64, P, P]
             L.oracle_mttkrp.argtypes = [i32, P, u64, P, P, i32, i32, P, P]
-            L.oracle_mttkrp_row.argtypes = [i32, u64, P, P, i32, i32, P, C.c_uint32, P]
             L.oracle_cholesky_solve.argtypes = [i32, P, u64, P, P]
             L.oracle_normalize.argtypes = [u64, i32, P, i32, P]
             L.oracle_fit.restype = f64
@@ -170,17 +169,6 @@ def mttkrp(dims, ind, vals, factors, mode):
     if st:
         raise OracleError(st)
     return M
-
-
-def mttkrp_row(ind, vals, factors, mode, i):
-    ind = _ind(ind)
-    v = np.ascontiguousarray(vals, dtype=np.float64)
-    fs = [np.ascontiguousarray(f, dtype=np.float64) for f in factors]
-    R = fs[0].shape[1]
-    out = np.empty(R)
-    lib().oracle_mttkrp_row(len(ind), v.shape[0], _ptrs(ind), _p(v), mode, R, _ptrs(fs),
-                            int(i), _p(out))
-    return out
 
 
 def cholesky_solve(V, M):

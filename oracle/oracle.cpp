@@ -163,24 +163,6 @@ int oracle_mttkrp(int N, const uint64_t* dims, uint64_t nnz, const uint32_t* con
     return OR_OK;
 }
 
-/* One output row, straight from the definition over ALL nonzeros (slow; used by
- * the full-size sampled parity tests).  out has R entries.                      */
-void oracle_mttkrp_row(int N, uint64_t nnz, const uint32_t* const* ind, const double* vals,
-                       int n, int R, const double* const* A, uint32_t i, double* out) {
-    std::vector<double> t(R);
-    for (int r = 0; r < R; ++r) out[r] = 0.0;
-    for (uint64_t p = 0; p < nnz; ++p) {
-        if (ind[n][p] != i) continue;
-        for (int r = 0; r < R; ++r) t[r] = vals[p];
-        for (int m = 0; m < N; ++m) {
-            if (m == n) continue;
-            const double* row = A[m] + (uint64_t)ind[m][p] * R;
-            for (int r = 0; r < R; ++r) t[r] = t[r] * row[r];
-        }
-        for (int r = 0; r < R; ++r) out[r] += t[r];
-    }
-}
-
 /* --------------------------------------------------------------- C-7 solve */
 /* Cholesky-Banachiewicz V = L L^T (no pivoting).  A pivot d_j <= 1e-12 * max_j V_jj
  * fails.  Returns 0 on success.                               */

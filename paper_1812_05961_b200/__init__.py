@@ -316,6 +316,13 @@ def _as_u32(a):
     if isinstance(a, np.ndarray):
         if a.dtype == np.int32 and a.flags.c_contiguous:
             return a.view(np.uint32)  # same bits, no copy (keeps pinned buffers pinned)
+        if a.dtype != np.uint32:
+            # narrowing a wider (or signed) integer type must not wrap out-of-range values
+            # into valid-looking indices that would bypass the library's BADINPUT check
+            if not np.issubdtype(a.dtype, np.integer):
+                raise TypeError("index arrays must have an integer dtype")
+            if a.size and (int(a.min()) < 0 or int(a.max()) >= (1 << 32)):
+                raise ValueError("index values must lie in [0, 2^32)")
         return np.ascontiguousarray(a, dtype=np.uint32)
     import torch
     if a.dtype == torch.int32 or a.dtype == torch.uint32:
@@ -446,6 +453,23 @@ def mttkrp(csf: Csf, mode: int, factors, out=None, rank: int | None = None,
     return out
 
 
+def _check_out_buffer(b, shape, ctx):
+    """A caller-supplied cpd_als output: the C side writes rank*8-byte rows with pitch
+    rank*8 into it, so it must be float64, C-contiguous, of exactly `shape`, and (CUDA
+    tensors) on the context's device."""
+    if isinstance(b, np.ndarray):
+        if b.dtype != np.float64 or not b.flags.c_contiguous or tuple(b.shape) != shape:
+            raise ValueError(f"out buffers must be C-contiguous float64 arrays of shape {shape}")
+        return
+    import torch
+    if not isinstance(b, torch.Tensor):
+        raise TypeError("out buffers must be numpy arrays or torch tensors")
+    if b.dtype != torch.float64 or not b.is_contiguous() or tuple(b.shape) != shape:
+        raise ValueError(f"out buffers must be contiguous float64 tensors of shape {shape}")
+    if b.is_cuda and b.device.index != ctx.device:
+        raise ValueError(f"out tensor on {b.device}, context on cuda:{ctx.device}")
+
+
 def _als_call(dims, rank, max_iters, init, ctx, out_device, stats, out, call):
     """Output buffers, initial factors and result dict shared by cpd_als / cpd_als_csf;
     `call(kr, init_arr, st)` performs the C call and returns its status."""
@@ -453,9 +477,10 @@ def _als_call(dims, rank, max_iters, init, ctx, out_device, stats, out, call):
     N = len(dims)
     if out is not None:  # caller buffers (host — e.g. pinned — or device), ld = rank
         fac, lam = list(out["factors"]), out["lam"]
-        for f, d in zip(fac, dims):
-            if tuple(f.shape) != (int(d), rank):
-                raise ValueError("out factor shape must be (I_n, rank)")
+        if len(fac) != N:
+            raise ValueError("out['factors'] must hold one buffer per mode")
+        for f, d in zip(fac + [lam], list(dims) + [None]):
+            _check_out_buffer(f, (int(d), rank) if d is not None else (rank,), ctx)
     elif out_device:
         fac = [torch.empty((int(d), rank), dtype=torch.float64, device=f"cuda:{ctx.device}")
                for d in dims]

@@ -3,6 +3,9 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -50,5 +53,19 @@ struct Error : std::runtime_error {
 inline int padded_ld(int R) { return (R + 3) / 4 * 4; }
 
 inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// Opt a kernel in to `bytes` of dynamic shared memory on the CURRENT device (the attribute is
+// per device: a process with contexts on several GPUs must set it on each).  Once per
+// (kernel, device); thread-safe (loopback ranks are threads).
+inline void set_max_dynamic_smem(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  SB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({kernel, dev})) return;
+  SB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert({kernel, dev});
+}
 
 }  // namespace sb

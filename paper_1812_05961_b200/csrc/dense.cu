@@ -5,10 +5,12 @@
 // (line 6), Gram refresh, and the fit (line 13).  Readings: DESIGN.md §2 (C-7 pivot
 // threshold / ridge, C-8 norm schedule, C-10 fit identity).
 //
-// Structure: one CTA factors V (right-looking Cholesky); persistent CTAs
-// solve tiles of rows in shared memory and, while a solved tile is still on chip, add
-// its partial Gram, column max |a| and fit inner product <M_i, A_i> = |L^-1 M_i|^2;
-// partials are reduced in a fixed order, so every result is deterministic.
+// Structure: one CTA forms V = *G and inverts it by Gauss-Jordan
+// elimination without pivoting (V is SPD; its k-th pivot is the k-th Cholesky pivot squared,
+// so the C-7 pivot test and ridge retry apply unchanged); persistent CTAs solve slabs of
+// rows X = M V^-1 (fp64 tensor cores, DMMA) and, while a solved slab is still on chip, add
+// its partial Gram, column max |a| and fit inner product <M_i, A_i>; partials are reduced
+// in a fixed order, so every result is deterministic.
 #include <algorithm>
 #include <cmath>
 
@@ -788,13 +790,7 @@ void hadamard_inverse(splatt_ctx* ctx, const double* G_all, int N, int n, int R,
                       double* Vinv, int* status, const double* sig, double* tau,
                       cudaStream_t stream) {
   const size_t smem = ((size_t)R * R + 2 * R) * sizeof(double);
-  static const bool attr_set = [] {  // thread-safe one-time init (loopback ranks are threads)
-    SB_CUDA(cudaFuncSetAttribute(hadamard_inverse_kernel,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (128 * 128 + 2 * 128) * 8));
-    return true;
-  }();
-  (void)attr_set;
+  set_max_dynamic_smem((const void*)hadamard_inverse_kernel, (128 * 128 + 2 * 128) * 8);
   hadamard_inverse_kernel<<<1, 1024, smem, stream ? stream : ctx->stream>>>(G_all, N, n, R, ld,
                                                                           Vinv, status, sig, tau,
                                                                           ctx->d_conv);
@@ -807,12 +803,7 @@ namespace {
 // (ld <= 60), else 256 (and 3 pairs per thread beyond 256 pairs, ld > 88).
 template <int KB, int G, int BT>
 void launch_rows(const RowsArgs& a, int P, size_t smem, cudaStream_t s) {
-  static const bool attr = [] {
-    SB_CUDA(cudaFuncSetAttribute(solve_gram_kernel<KB, G, BT>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    return true;
-  }();
-  (void)attr;
+  set_max_dynamic_smem((const void*)solve_gram_kernel<KB, G, BT>, 200 * 1024);
   solve_gram_kernel<KB, G, BT><<<P, BT, smem, s>>>(a);
 }
 
@@ -835,12 +826,7 @@ constexpr int mma_warps(int NT) { return NT <= 5 ? SB_MMA_W : 8; }
 template <int NT>
 void launch_rows_mma_t(const RowsArgs& a, int P, size_t smem, cudaStream_t s) {
   constexpr int W = mma_warps(NT);
-  static const bool attr = [] {
-    SB_CUDA(cudaFuncSetAttribute(solve_gram_mma_kernel<NT, W>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    return true;
-  }();
-  (void)attr;
+  set_max_dynamic_smem((const void*)solve_gram_mma_kernel<NT, W>, 220 * 1024);
   solve_gram_mma_kernel<NT, W><<<P, W * 32, smem, s>>>(a);
 }
 

@@ -601,12 +601,7 @@ void launch_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, doub
   while (threads > 64 && smem_for(threads) > 160 * 1024) threads /= 2;
   const int groups_per_block = Lanes<G>::groups_per_block(threads);
   const size_t smem = smem_for(threads);
-  static const bool attr = [] {  // thread-safe one-time init (loopback ranks are threads)
-    SB_CUDA(cudaFuncSetAttribute(mttkrp_csf_kernel<N, D, G, U, MINB, L1A>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    return true;
-  }();
-  (void)attr;
+  set_max_dynamic_smem((const void*)mttkrp_csf_kernel<N, D, G, U, MINB, L1A>, 160 * 1024);
   uint64_t blocks = ceil_div(c.nchunks, groups_per_block);
   static const bool dyn_env = [] {
     const char* e = getenv("SPLATT_DYN");

@@ -39,6 +39,23 @@ def test_reference_arm_line():
     assert e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
 
 
+def test_self_launch_two_ranks():
+    """`bench.py --gpus 2` outside torchrun re-executes itself under torch.distributed.run with
+    two ranks on 127.0.0.1 (what a driver's `bench.py --gpus 8` relies on); rank 0 alone prints
+    the line.  The reference arm runs without a GPU, so the launcher is checked on CPU."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--gpus", "2", "--config", "c1", "--steps", "1", "--warmup", "0"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["world_size"] == 2 and d["n_gpus"] == 2 and d["impl"] == "reference"
+    assert "torch.distributed.run" in out.stderr
+
+
 def test_gather_view_helper():
     sys.path.insert(0, ROOT)
     import bench
@@ -66,5 +83,8 @@ def test_our_arm_line(cuda_ok):
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0
+    assert d["comm"]["nranks"] == 1
+    assert {"alg_frac_of_hbm", "dram_frac_of_hbm", "l1tex_wavefront_pct"} <= set(r["views"])
+    assert "one_thread" in cb and cb["one_thread"]["value"] > 0 and cb["host"]["logical_cpus"]
     clk = d["clocks"]
     assert clk is None or {"sm_mhz", "sm_max_mhz", "reasons"} <= set(clk)

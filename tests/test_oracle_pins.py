@@ -148,6 +148,48 @@ def test_x5_singular_and_ridge():
     assert np.all(np.isfinite(X))
 
 
+def test_x5_ridge_magnitude_closed_form():
+    """C-7 / Q-14 ridge size, pinned by closed forms: a PSD V whose first
+    Cholesky attempt fails is retried as W = V + delta I with delta = 1e-12 trace(V) / R.
+    With m along V's null vector u (V u = 0), x W = m has the closed-form solution
+    x = m / delta, so x measures delta itself."""
+    # V = [[1,1],[1,1]]: pivot 2 is exactly 0 -> ridge delta = 1e-12 * 2 / 2 = 1e-12;
+    # u = [1,-1]: x = [1,-1] / 1e-12.
+    X = oracle.cholesky_solve(np.array([[1.0, 1.0], [1.0, 1.0]]), np.array([[1.0, -1.0]]))
+    assert np.allclose(X[0], [1e12, -1e12], rtol=1e-3, atol=0)
+    # Unequal diagonal, so trace/R (= 2.5/3) differs from the max diagonal (1) and from the
+    # trace (2.5): delta = 1e-12 * 2.5 / 3 -> x = [1,-1,0] / delta = [1.2e12, -1.2e12, 0].
+    # (1e-12 * max diag would give 1e12, 1e-12 * trace 4e11.)
+    V = np.array([[1.0, 1.0, 0.0], [1.0, 1.0, 0.0], [0.0, 0.0, 0.5]])
+    X = oracle.cholesky_solve(V, np.array([[1.0, -1.0, 0.0]]))
+    delta = 1e-12 * 2.5 / 3
+    assert np.allclose(X[0], [1 / delta, -1 / delta, 0.0], rtol=1e-3, atol=1e-3)
+    # A ridge too small to rescue: V = [[4,2],[2,1]] (null vector [1,-2]).  delta = 2.5e-12,
+    # the retried pivot is delta + delta/(4+delta) = 1.25 delta = 3.1e-12 <= 1e-12 * (4 + delta)
+    # -> SINGULAR.  A ridge of 1e-12 * trace (5e-12) or 1e-12 * max diag (4e-12) would pass.
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.cholesky_solve(np.array([[4.0, 2.0], [2.0, 1.0]]), np.array([[1.0, 1.0]]))
+    assert e.value.code == oracle.SINGULAR
+
+
+def test_x5_pivot_threshold_closed_form():
+    """Q-14 pivot threshold: a pivot d fails iff d <= 1e-12 * max_j V_jj.  V = [[1,1],[1,1+a]]
+    has second pivot exactly a (1 + a - 1, Sterbenz), and for m = [0, 1]:
+      no ridge:   x = m V^-1 = [-1, 1] / a
+      with ridge: x = [-1, 1 + delta] / ((1+delta)(1+a+delta) - 1),  delta = 1e-12 (2+a)/2."""
+    for a, ridged in ((1.1e-12, False), (2e-12, False), (0.9e-12, True), (0.5e-12, True)):
+        V = np.array([[1.0, 1.0], [1.0, 1.0 + a]])
+        a_eff = (1.0 + a) - 1.0  # the representable a
+        X = oracle.cholesky_solve(V, np.array([[0.0, 1.0]]))[0]
+        if ridged:
+            d = 1e-12 * (2.0 + a_eff) / 2.0
+            det = (1 + d) * (1 + a_eff + d) - 1
+            ref = np.array([-1.0, 1.0 + d]) / det
+        else:
+            ref = np.array([-1.0, 1.0]) / a_eff
+        assert np.allclose(X, ref, rtol=1e-3, atol=0), (a, X, ref)
+
+
 def test_x5_one_mode_update_is_least_squares():
     """One ALS mode update = argmin_A ||X_(n) - A K^T||_F on the dense unfolding."""
     rng = np.random.default_rng(9)
