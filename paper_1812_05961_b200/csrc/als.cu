@@ -515,7 +515,9 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   if (max_iters >= 5 && !getenv("SPLATT_L1_ALLOC")) {
     for (int n = 0; n < N; ++n) {
       const DevCsf& cn = *csf[mode_csf[n]];
-      tune[n] = mode_level[n] == 0 && cn.l1a < 0 && cn.nnz >= (1u << 20);
+      // (the second-generation ROOT kernel has one gather policy: nothing to time)
+      tune[n] = mode_level[n] == 0 && cn.l1a < 0 && cn.nnz >= (1u << 20) &&
+                !root2_eligible(ctx, cn, ld);
       if (tune[n]) {
         tuning = true;
         for (int e = 0; e < 4; ++e) SB_CUDA(cudaEventCreate(&tev[n][e]));

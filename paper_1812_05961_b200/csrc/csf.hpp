@@ -12,6 +12,18 @@ namespace sb {
 #endif
 constexpr int kHotRows = SB_HOT_ROWS;
 
+// Per-tree plan of the second-generation ROOT MTTKRP (root2.cu / root2.cuh): per-leaf
+// records {leaf code | d << 29, closing fiber's code, value}, coded ids of levels 1..N-3 and
+// the K (level, id) rows held in shared memory.  Built for one padded rank `ld` (K depends
+// on the row size).
+struct RootPlan {
+  int ld = 0;
+  uint32_t K = 0;
+  DevBuf<uint4> rec;
+  DevBuf<uint32_t> cid[SPLATT_MAX_NMODES];
+  DevBuf<uint32_t> hot;
+};
+
 // One CSF tree.  Level l < N-1: ids[l] (nodes[l]) and ptr[l] (nodes[l]+1, offsets into
 // level l+1); leaf level N-1: ids[N-1] (nnz) and vals (nnz).  perm[l] = mode at level l.
 struct DevCsf {
@@ -55,6 +67,7 @@ struct DevCsf {
   // lazily (chunk table, seam rows, tiles) come from the same one, so they live as long as
   // the tree: a call-arena tree dies with its call, a splatt_csf_build tree with its handle.
   Arena* arena = nullptr;
+  std::unique_ptr<RootPlan> plan;  // ROOT kernel v2 (built on first use, mttkrp_prepare)
 };
 
 // Split c by leaf id into T tiles of ceil(I_leaf / T) ids (tiles empty of nonzeros skipped).

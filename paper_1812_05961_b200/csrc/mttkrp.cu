@@ -240,10 +240,14 @@ void mttkrp_prepare(splatt_ctx* ctx, DevCsf& c, int level, int ld) {
   if (level == 0) {
     const int T = leaf_tiles(ctx, c, ld);
     if (T > 1 && c.tiles.empty()) tile_tree(ctx, c, T);
-    for (auto& t : c.tiles) ensure_chunk_table(ctx, *t, mttkrp_chunk_leaves(*t));
+    for (auto& t : c.tiles) {
+      ensure_chunk_table(ctx, *t, mttkrp_chunk_leaves(*t));
+      if (t->nnz && root2_eligible(ctx, *t, ld)) ensure_root_plan(ctx, *t, ld);
+    }
     if (!c.tiles.empty()) return;
   }
   ensure_chunk_table(ctx, c, mttkrp_chunk_leaves(c));
+  if (level == 0 && root2_eligible(ctx, c, ld)) ensure_root_plan(ctx, c, ld);
   if (level > 0) ensure_hot(ctx, c, level);
 }
 
@@ -260,6 +264,10 @@ void mttkrp_level(splatt_ctx* ctx, DevCsf& c, int level, const double* const* fa
   auto launch = [&](DevCsf& t, int accumulate) {
     accumulate |= l1a;
     const int chunk = (int)t.tab_chunk;  // the tree's chunk table (mttkrp_prepare)
+    if (level == 0 && t.plan && t.plan->ld == ld && root2_eligible(ctx, t, ld)) {
+      mttkrp_root2_launch(ctx, t, fac_by_mode, out, ld, R, accumulate & 1);
+      return;
+    }
     switch (c.N) {
       case 3: mttkrp_launch_n3(ctx, t, level, fac_by_mode, out, ld, R, chunk, accumulate); break;
       case 4: mttkrp_launch_n4(ctx, t, level, fac_by_mode, out, ld, R, chunk, accumulate); break;

@@ -34,6 +34,14 @@ double mttkrp_alg_bytes(const DevCsf& c, int R, int level = 0);
 // distinct[m] = rows of mode m the tensor references (or an upper bound).
 double mttkrp_min_bytes(const DevCsf& c, int R, int level, const uint64_t* distinct);
 
+// Second-generation ROOT kernel (root2.cu): whether tree `c` runs it (N = 3, 4; non-root
+// level dims < 2^28; not in deterministic mode; SPLATT_ROOT2=0 disables it), its plan, and
+// its launch (acc bit 0: add into the owned rows).
+bool root2_eligible(const splatt_ctx* ctx, const DevCsf& c, int ld);
+void ensure_root_plan(splatt_ctx* ctx, DevCsf& c, int ld);
+void mttkrp_root2_launch(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode,
+                         double* out, int ld, int R, int acc);
+
 // Leaves per ROOT/INTERNAL/LEAF work unit of tree `c` (its chunk table's granularity).
 int mttkrp_chunk_leaves(const DevCsf& c);
 

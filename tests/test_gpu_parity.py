@@ -383,3 +383,51 @@ def test_mttkrp_leaf_tiling(sb, ctx):
         als_compare(res, ref)
     res = sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=5, seed=3, ctx=ctx)  # + gather tuning
     als_compare(res, oracle.cpd_als(t.dims, t.ind, t.vals, rank=R, max_iters=5, seed=3))
+
+
+@pytest.mark.parametrize("R", [3, 16, 35, 64])
+def test_root_kernel_generations_agree(sb, ctx, monkeypatch, R):
+    """The second-generation ROOT kernel (records + shared-memory hot rows, root2.cuh) and
+    the first (mttkrp_kernel.cuh, SPLATT_ROOT2=0) against the oracle on power-law tensors
+    (N = 3 and 4), where the hot-row table takes most gathers."""
+    import torch
+    for idx, (dims, nnz, dists) in enumerate([((3000, 800, 5000), 200_000, [("zipf", 1.1)] * 3),
+                                              ((2000, 700, 300, 40), 150_000, [("zipf", 1.05)] * 4)]):
+        t = synth.generate(dims, nnz, dists, "u01", seed=50 + idx)
+        F = oracle.init_factors(t.dims, R, 7)
+        ind, vals = dev_coo(t)
+        fd = dev_factors(F, sb.padded_ld(R))
+        for env in ("3", "0"):  # second generation (also on N = 3), first generation
+            monkeypatch.setenv("SPLATT_ROOT2", env)
+            csf = sb.csf_build(ind, vals, t.dims, ctx=ctx)
+            for n in range(t.nmodes):
+                M = sb.mttkrp(csf, n, fd, rank=R).cpu().numpy()[:, :R]
+                ref = oracle.mttkrp(t.dims, t.ind, t.vals, F, n)
+                assert rel_fro(M, ref) <= MTTKRP_TOL, (env, n)
+            del csf
+        torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("chunk", ["32", "96", "1024"])
+def test_root2_four_mode_seams_and_tiles(sb, monkeypatch, chunk):
+    """4-mode ROOT kernel v2 with tiny and default chunks (every kind of seam: slices,
+    level-1 nodes and fibers cut by chunk ends, heavy slices over many chunks) and with forced
+    leaf tiles (later tiles add into the owned rows), against the oracle."""
+    monkeypatch.setenv("SPLATT_CHUNK", chunk)
+    # >= 2^20 nonzeros: leaf tiling applies (the 90000-row leaf factor -> 8 tiles at 1e-4)
+    t = synth.generate((60, 3000, 40, 90000), 1_100_000,
+                       [("zipf", 1.3), ("zipf", 1.05), ("zipf", 1.2), ("uniform",)], "u01", seed=71)
+    R = 16
+    F = oracle.init_factors(t.dims, R, 3)
+    ind, vals = dev_coo(t)
+    fd = dev_factors(F, sb.padded_ld(R))
+    for tiling in (0.0, 1e-4):
+        c = sb.Context(0)
+        c.set_leaf_tiling(tiling)
+        csf = sb.csf_build(ind, vals, t.dims, ctx=c)
+        for n in range(4):
+            M = sb.mttkrp(csf, n, fd, rank=R).cpu().numpy()[:, :R]
+            ref = oracle.mttkrp(t.dims, t.ind, t.vals, F, n)
+            assert rel_fro(M, ref) <= MTTKRP_TOL, (tiling, n)
+        del csf
+        c.close()
