@@ -268,7 +268,13 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       owned[k] = std::make_unique<DevCsf>();
       csf[k] = owned[k].get();
     }
+    struct PlanScope {  // ROOT plans formed during the build (policy ALL: every tree ROOT)
+      splatt_ctx* c;
+      ~PlanScope() { c->build_plan_ld = 0; }
+    } plan_scope{ctx};
+    ctx->build_plan_ld = (policy == SPLATT_CSF_ALL) ? ld : 0;
     build_csf_set(ctx, X.ind, X.vals, X.nnz, N, X.dims, roots, ncsf, csf.data());
+    ctx->build_plan_ld = 0;
     for (int n = 0; n < N; ++n)
       if (mode_level[n] > 0) csf[mode_csf[n]]->nonroot = true;
     if (late_norm) {
@@ -367,7 +373,14 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     const uint32_t* lp[SPLATT_MAX_NMODES];
     for (int m = 0; m < N; ++m) lp[m] = lind[m].p;
     ArenaScope back(call_arena, false);
-    build_csf(ctx, lp, lval.p, local, N, X.dims, n, *csf[n]);
+    ctx->build_plan_ld = ld;  // sharded: every local tree runs ROOT
+    try {
+      build_csf(ctx, lp, lval.p, local, N, X.dims, n, *csf[n]);
+    } catch (...) {
+      ctx->build_plan_ld = 0;
+      throw;
+    }
+    ctx->build_plan_ld = 0;
   }
   for (int n = 0; n < N; ++n)  // chunk tables / hot ids before the loop (no syncs inside it)
     mttkrp_prepare(ctx, *csf[sharded ? n : mode_csf[n]], sharded ? 0 : mode_level[n], ld);

@@ -416,6 +416,15 @@ void finish_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& 
     SB_CHECK_LAUNCH(ctx);
   }
   tr.mark("scatter");
+  if (ctx->build_plan_ld > 0) {
+    const uint32_t* cp[SPLATT_MAX_NMODES];
+    const uint32_t* np[SPLATT_MAX_NMODES];
+    for (int l = 0; l < N; ++l) cp[l] = t.coord[l].p;
+    for (int l = 0; l < N - 1; ++l) np[l] = node[l].p;
+    ArenaScope o(out_arena, false);  // the plan lives as long as the tree
+    root_plan_from_levels(ctx, out, cp, np, t.vals.p, ctx->build_plan_ld);
+    tr.mark("root plan");
+  }
   out.ids[N - 1] = std::move(t.coord[N - 1]);
   out.vals = std::move(t.vals);
   out.tab_chunk = 0;

@@ -98,6 +98,13 @@ void build_csf_set(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* 
                    uint64_t nnz, int N, const uint64_t* dims, const int* roots, int ntrees,
                    DevCsf* const* outs);
 
+// Second-generation ROOT plan of tree `out` for padded rank `ld`, from the builder's
+// level-order sorted coordinates coord[l][k] and inclusive node numbering node[l][k]
+// (1 + index of the level-l node containing leaf k, l < N-1) and the sorted values: no
+// walk over the tree's ptr arrays (root2.cu).  No-op unless root2 applies to `out`.
+void root_plan_from_levels(splatt_ctx* ctx, DevCsf& out, const uint32_t* const* coord,
+                           const uint32_t* const* node, const double* vals, int ld);
+
 // Ensure the chunk table for `chunk` leaves per work unit exists.
 void ensure_chunk_table(splatt_ctx* ctx, DevCsf& c, int chunk);
 

@@ -43,6 +43,10 @@ struct splatt_ctx {
   int part_mode = SPLATT_PART_AUTO;    // sharded path: P1 / P2 per mode (SPLATT_PART_*)
   double leaf_tile_frac = -1.0;        // ROOT MTTKRP leaf tiling (0 = off, < 0 = auto)
   bool deterministic = false;          // ROOT MTTKRP seams: fixed-order sums, no atomics
+  // While a cpd_als call builds trees that only run ROOT traversals (policy ALL): the padded
+  // rank their second-generation ROOT plans are for; the builder then forms the plan from the
+  // sorted coordinates it already holds (root2.cu, root_plan_from_levels).  0 = no plan.
+  int build_plan_ld = 0;
   // During an ALS call with tol > 0: device int, the iteration at which the fit stopped
   // improving (0 = still running).  Kernels of the loop return at once when it is set, so
   // the host enqueues iterations ahead without a sync per iteration (nullptr otherwise).

@@ -29,7 +29,10 @@ inline int grid_n(splatt_ctx* ctx, uint64_t n) {
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(n, 256), (uint64_t)ctx->num_sms * 16));
 }
 
-constexpr uint32_t kSample = 16;  // histogram: every 16th node / leaf
+#ifndef SB_PLAN_SAMPLE
+#define SB_PLAN_SAMPLE 64
+#endif
+constexpr uint32_t kSample = SB_PLAN_SAMPLE;  // histogram: every kSample-th node / leaf
 
 __global__ void sampled_hist_kernel(const uint32_t* __restrict__ ids, uint64_t n, uint32_t step,
                                     uint32_t* __restrict__ cnt) {
@@ -112,6 +115,56 @@ __global__ void code_level_kernel(const uint32_t* __restrict__ ids, uint64_t n,
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
        j += (uint64_t)gridDim.x * blockDim.x)
     out[j] = code_of(slotmap, off, ids[j], ldb);
+}
+
+struct LevelArrays {
+  const uint32_t* coord[SPLATT_MAX_NMODES];  // level-order sorted coordinates (nnz each)
+  const uint32_t* node[SPLATT_MAX_NMODES];   // inclusive node numbering, levels 0..N-2
+  int N;
+};
+
+__device__ __forceinline__ bool node_starts(const LevelArrays& la, int l, uint64_t k) {
+  return k == 0 || la.node[l][k] != la.node[l][k - 1];
+}
+
+// Every kSample-th leaf: its id, and the id of every internal node (levels 1..N-2) that
+// starts there (each node has one start, so nodes are sampled at the same 1/kSample rate).
+__global__ void sampled_hist_levels_kernel(LevelArrays la, uint64_t nnz, LevelOffsets lo,
+                                           uint32_t* __restrict__ cnt) {
+  const int N = la.N;
+  for (uint64_t k = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * kSample; k < nnz;
+       k += (uint64_t)gridDim.x * blockDim.x * kSample) {
+    atomicAdd(&cnt[lo.off[N - 1] + la.coord[N - 1][k]], 1u);
+    for (int l = 1; l <= N - 2; ++l)
+      if (node_starts(la, l, k)) atomicAdd(&cnt[lo.off[l] + la.coord[l][k]], 1u);
+  }
+}
+
+// Records and coded node ids in one pass over the leaves: d = the shallowest level whose
+// node ends at leaf k (node numbering changes at k+1, or k is the last leaf); a level-l node
+// (l <= N-3) that starts at k writes its id (level 0) or code into cid[l].
+struct CidOut { uint32_t* cid[SPLATT_MAX_NMODES]; };
+__global__ void records_from_levels_kernel(LevelArrays la, const double* __restrict__ vals,
+                                           uint64_t nnz, const uint32_t* __restrict__ slotmap,
+                                           LevelOffsets lo, uint32_t ldb, CidOut co,
+                                           uint4* __restrict__ rec) {
+  const int N = la.N;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t d = (uint32_t)(N - 1);
+    for (int l = N - 2; l >= 0; --l)
+      if (k + 1 == nnz || la.node[l][k + 1] != la.node[l][k]) d = (uint32_t)l;
+    const uint32_t code = code_of(slotmap, lo.off[N - 1], la.coord[N - 1][k], ldb);
+    const uint32_t fcode =
+        d <= (uint32_t)(N - 2) ? code_of(slotmap, lo.off[N - 2], la.coord[N - 2][k], ldb) : 0u;
+    const double v = vals[k];
+    rec[k] = make_uint4(code | (d << r2::kDShift), fcode, (uint32_t)__double2loint(v),
+                        (uint32_t)__double2hiint(v));
+    for (int l = 0; l <= N - 3; ++l)
+      if (node_starts(la, l, k))
+        co.cid[l][la.node[l][k] - 1] =
+            l == 0 ? la.coord[0][k] : code_of(slotmap, lo.off[l], la.coord[l][k], ldb);
+  }
 }
 
 template <int G>
@@ -228,6 +281,62 @@ void ensure_root_plan(splatt_ctx* ctx, DevCsf& c, int ld) {
                                                                   plan->cid[l].p);
       SB_CHECK_LAUNCH(ctx);
     }
+  }
+  c.plan = std::move(plan);
+}
+
+void root_plan_from_levels(splatt_ctx* ctx, DevCsf& c, const uint32_t* const* coord,
+                           const uint32_t* const* node, const double* vals, int ld) {
+  if (c.nnz == 0 || !root2_eligible(ctx, c, ld)) return;
+  cudaStream_t st = ctx->stream;
+  const int N = c.N;
+  auto plan = std::make_unique<RootPlan>();  // from the current arena (the tree's)
+  plan->ld = ld;
+  plan->K = root2_hot_capacity(N, ld);
+  if (const char* e = getenv("SPLATT_ROOT2_HOT")) plan->K = std::min<uint32_t>(plan->K, atoi(e));
+  const uint32_t ldb = (uint32_t)ld * 8u;
+  LevelOffsets lo{};
+  lo.N = N;
+  uint64_t total = 0;
+  for (int l = 1; l < N; ++l) { lo.off[l] = total; total += c.dims[l]; }
+  lo.off[N] = total;
+  plan->rec.alloc(c.nnz, st);
+  CidOut co{};
+  for (int l = 0; l <= N - 3; ++l) {
+    plan->cid[l].alloc(c.nodes[l] + 1, st);
+    SB_CUDA(cudaMemsetAsync(plan->cid[l].p + c.nodes[l], 0, 4, st));
+    co.cid[l] = plan->cid[l].p;
+  }
+  plan->hot.alloc(std::max<uint32_t>(1, plan->K), st);
+  LevelArrays la{};
+  la.N = N;
+  for (int l = 0; l < N; ++l) la.coord[l] = coord[l];
+  for (int l = 0; l < N - 1; ++l) la.node[l] = node[l];
+  {
+    ArenaScope tmp(current_arena(), true);
+    DevBuf<uint32_t> cnt(total, st), cnt2(total, st), gidx(total, st), gidx2(total, st),
+        slotmap(total, st);
+    SB_CUDA(cudaMemsetAsync(cnt.p, 0, total * 4, st));
+    SB_CUDA(cudaMemsetAsync(slotmap.p, 0xff, total * 4, st));
+    sampled_hist_levels_kernel<<<grid_n(ctx, ceil_div(c.nnz, kSample)), 256, 0, st>>>(
+        la, c.nnz, lo, cnt.p);
+    SB_CHECK_LAUNCH(ctx);
+    iota_u32_kernel<<<grid_n(ctx, total), 256, 0, st>>>(gidx.p, total);
+    SB_CHECK_LAUNCH(ctx);
+    size_t tb = 0;
+    SB_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cnt.p, cnt2.p, gidx.p, gidx2.p,
+                                                      (int)total, 0, 32, st));
+    DevBuf<uint8_t> temp(tb, st);
+    SB_CUDA(cub::DeviceRadixSort::SortPairsDescending(temp.p, tb, cnt.p, cnt2.p, gidx.p, gidx2.p,
+                                                      (int)total, 0, 32, st));
+    if (plan->K > 0) {
+      hot_slots_kernel<<<(unsigned)ceil_div(plan->K, 256), 256, 0, st>>>(
+          cnt2.p, gidx2.p, total, plan->K, lo, plan->hot.p, slotmap.p);
+      SB_CHECK_LAUNCH(ctx);
+    }
+    records_from_levels_kernel<<<grid_n(ctx, c.nnz), 256, 0, st>>>(la, vals, c.nnz, slotmap.p, lo,
+                                                                   ldb, co, plan->rec.p);
+    SB_CHECK_LAUNCH(ctx);
   }
   c.plan = std::move(plan);
 }

@@ -54,7 +54,8 @@ struct Threads { static constexpr int k = (N == 3) ? SB_ROOT2_THREADS3 : SB_ROOT
 #ifndef SB_ROOT2_B
 #define SB_ROOT2_B 48
 #endif
-constexpr int kB = SB_ROOT2_B;              // leaves per staged batch
+constexpr int kBMax = SB_ROOT2_B;           // leaves per staged batch (at most)
+constexpr int kRecBudget = 200 * 1024;      // record buffers of all groups of a CTA (at most)
 constexpr int kSmemBudget = 225 * 1024;     // dynamic shared memory per CTA
 
 struct d4 { double x, y, z, w; };
@@ -174,10 +175,21 @@ struct Lanes {
 
 // Shared memory: [hot rows: K x ld doubles][per group: 2 x kB records + 16-byte skew].
 // The skew puts the same record index of the groups sharing a warp into different bank
-// windows (their broadcast reads then share a wavefront).
-constexpr int kGroupRecBytes = 2 * kB * 16 + 16;
+// windows (their broadcast reads then share a wavefront).  kB: the largest batch (48 on
+// B200 sweeps, profiles/ab_r02/) whose buffers for every group fit kRecBudget (narrow groups
+// are many per CTA).
+constexpr int group_rec_bytes(int b) { return 2 * b * 16 + 16; }
 template <int G, int T>
-__host__ __device__ constexpr int rec_smem_bytes() { return Lanes<G, T>::kGroups * kGroupRecBytes; }
+__host__ __device__ constexpr int batch_leaves() {
+  return Lanes<G, T>::kGroups * group_rec_bytes(kBMax) <= kRecBudget ? kBMax
+       : Lanes<G, T>::kGroups * group_rec_bytes(32) <= kRecBudget    ? 32
+       : Lanes<G, T>::kGroups * group_rec_bytes(16) <= kRecBudget    ? 16
+                                                                      : 8;
+}
+template <int G, int T>
+__host__ __device__ constexpr int rec_smem_bytes() {
+  return Lanes<G, T>::kGroups * group_rec_bytes(batch_leaves<G, T>());
+}
 template <int G, int T>
 inline uint32_t hot_capacity(int ld) {
   const long free_b = (long)kSmemBudget - rec_smem_bytes<G, T>();
@@ -187,6 +199,8 @@ inline uint32_t hot_capacity(int ld) {
 template <int N, int G, int U>
 __global__ void __launch_bounds__(Threads<N>::k, 1) mttkrp_root2_kernel(const Args<N> a) {
   using L = Lanes<G, Threads<N>::k>;
+  constexpr int kB = batch_leaves<G, Threads<N>::k>();
+  constexpr int kGroupRecBytes = group_rec_bytes(kB);
   extern __shared__ __align__(16) unsigned char smem2[];
   if (a.conv && *a.conv) return;
   double* hotrows = reinterpret_cast<double*>(smem2);
