@@ -525,6 +525,22 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   auto& tev = tev_own.e;
   bool tune[SPLATT_MAX_NMODES] = {false};
   bool tuning = false;
+  auto memo_key = [&](const DevCsf& c) {
+    std::vector<uint64_t> k{(uint64_t)c.N, (uint64_t)ld, c.nnz, (uint64_t)c.tiles.size()};
+    for (int l = 0; l < c.N; ++l) {
+      k.push_back((uint64_t)c.perm[l]);
+      k.push_back(c.dims[l]);
+      k.push_back(c.nodes[l]);
+    }
+    return k;
+  };
+  for (int n = 0; n < N; ++n) {  // a policy an earlier call timed on the same tree shape
+    DevCsf& cn = *csf[mode_csf[n]];
+    if (mode_level[n] == 0 && cn.l1a < 0) {
+      auto it = ctx->l1a_memo.find(memo_key(cn));
+      if (it != ctx->l1a_memo.end()) cn.l1a = it->second;
+    }
+  }
   if (max_iters >= 5 && !getenv("SPLATT_L1_ALLOC")) {
     for (int n = 0; n < N; ++n) {
       const DevCsf& cn = *csf[mode_csf[n]];
@@ -612,6 +628,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
         SB_CUDA(cudaEventElapsedTime(&t0, tev[n][0], tev[n][1]));
         SB_CUDA(cudaEventElapsedTime(&t1, tev[n][2], tev[n][3]));
         csf[mode_csf[n]]->l1a = (t1 < t0) ? 1 : 0;
+        ctx->l1a_memo[memo_key(*csf[mode_csf[n]])] = csf[mode_csf[n]]->l1a;
         if (getenv("SPLATT_TRACE"))
           fprintf(stderr, "[splatt] mode %d ROOT gathers: no_allocate %.3f ms, L1-allocating %.3f ms\n",
                   n, t0, t1);

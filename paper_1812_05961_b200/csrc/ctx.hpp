@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <map>
 #include <memory>
 #include <string>
 #include <utility>
@@ -47,6 +48,10 @@ struct splatt_ctx {
   // rank their second-generation ROOT plans are for; the builder then forms the plan from the
   // sorted coordinates it already holds (root2.cu, root_plan_from_levels).  0 = no plan.
   int build_plan_ld = 0;
+  // ROOT gather cache policy chosen by an earlier cpd_als call, keyed by the
+  // tree's shape (order, rank padding, nonzeros, node counts, tiles): a repeated call on the
+  // same tensor skips the timing iterations and their host sync.
+  std::map<std::vector<uint64_t>, int> l1a_memo;
   // During an ALS call with tol > 0: device int, the iteration at which the fit stopped
   // improving (0 = still running).  Kernels of the loop return at once when it is set, so
   // the host enqueues iterations ahead without a sync per iteration (nullptr otherwise).
