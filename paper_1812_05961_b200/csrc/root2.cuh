@@ -305,62 +305,67 @@ __global__ void __launch_bounds__(Threads<N>::k, 1) mttkrp_root2_kernel(const Ar
       }
       __syncwarp(gmask);
       const uint32_t rb_sa = rec_sa + (uint32_t)which * (kB * 16u);
-      for (uint32_t t0 = 0; t0 < nb; t0 += U) {
-        d4 row[U], frow[U];
-        uint32_t dd[U];
-        double v[U];
+      // One leaf: its record (shared memory) and gathered rows.  Past the batch end the
+      // last record is re-read and made inert (v = 0, no close, no gathers).
+      struct Leaf { d4 row, frow; uint32_t d; double v; };
+      auto fetch = [&](uint32_t t) -> Leaf {
+        const bool valid = t < nb;
+        const uint4 r = lds_u4(rb_sa + 16u * min(t, nb - 1));
+        Leaf f;
+        f.d = valid ? (r.x >> kDShift) : (uint32_t)(N - 1);
+        f.v = valid ? __hiloint2double((int)r.w, (int)r.z) : 0.0;
+        f.row = gather_en(N - 1, r.x & (kHot | kIdMask), valid);
+        f.frow = gather_en(N - 2, r.y, f.d <= (uint32_t)(N - 2));
+        return f;
+      };
+      auto consume = [&](const Leaf& f, bool valid) {
+        const uint32_t d = f.d;
+        if (valid) fma4(acc[N - 2], f.v, f.row);
+        if (d <= (uint32_t)(N - 2)) {
+          fma4v(acc[N - 3], acc[N - 2], f.frow);
+          acc[N - 2] = d4{0, 0, 0, 0};
+          ++nfib;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          // past the batch end: a re-read of the last record, made inert (v = 0, no close)
-          const bool valid = t0 + u < nb;
-          const uint32_t t = min(t0 + u, nb - 1);
-          const uint4 r = lds_u4(rb_sa + 16u * t);
-          dd[u] = valid ? (r.x >> kDShift) : (uint32_t)(N - 1);
-          v[u] = valid ? __hiloint2double((int)r.w, (int)r.z) : 0.0;
-          row[u] = gather(N - 1, r.x & (kHot | kIdMask));
-          frow[u] = gather_en(N - 2, r.y, dd[u] <= (uint32_t)(N - 2));
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t d = dd[u];
-          fma4(acc[N - 2], v[u], row[u]);
-          if (d <= (uint32_t)(N - 2)) {
-            fma4v(acc[N - 3], acc[N - 2], frow[u]);
-            acc[N - 2] = d4{0, 0, 0, 0};
-            ++nfib;
-#pragma unroll
-            for (int l = N - 3; l >= 1; --l) {
-              if (d <= (uint32_t)l) {
-                fma4v(acc[l - 1], acc[l], mrow[l - 1]);
-                acc[l] = d4{0, 0, 0, 0};
-                ++base[l];
-                mrow[l - 1] = gather(l, nid[l - 1]);
-                nid[l - 1] = ld_u32(a.cid[l] + base[l] + 1);
-              }
-            }
-            if (d == 0) {
-              double* dst = a.out + (size_t)rid * ld + col;
-              d4 r = mask_pad(acc[0], col, a.R);
-              if (active) {
-                if (head) {
-                  atomic_row(dst, r);
-                } else {
-                  if (a.accumulate) {
-                    const d4 o = d4{dst[0], dst[1], dst[2], dst[3]};
-                    r = d4{r.x + o.x, r.y + o.y, r.z + o.z, r.w + o.w};
-                  }
-                  st_row(dst, r);
-                }
-              }
-              head = false;
-              acc[0] = d4{0, 0, 0, 0};
-              ++base[0];
-              rid = nrid;
-              nrid = ld_u32(a.cid[0] + base[0] + 1);
+          for (int l = N - 3; l >= 1; --l) {
+            if (d <= (uint32_t)l) {
+              fma4v(acc[l - 1], acc[l], mrow[l - 1]);
+              acc[l] = d4{0, 0, 0, 0};
+              ++base[l];
+              mrow[l - 1] = gather(l, nid[l - 1]);
+              nid[l - 1] = ld_u32(a.cid[l] + base[l] + 1);
             }
           }
-          if (t0 + u < nb) last_d = d;
+          if (d == 0) {
+            double* dst = a.out + (size_t)rid * ld + col;
+            d4 r = mask_pad(acc[0], col, a.R);
+            if (active) {
+              if (head) {
+                atomic_row(dst, r);
+              } else {
+                if (a.accumulate) {
+                  const d4 o = d4{dst[0], dst[1], dst[2], dst[3]};
+                  r = d4{r.x + o.x, r.y + o.y, r.z + o.z, r.w + o.w};
+                }
+                st_row(dst, r);
+              }
+            }
+            head = false;
+            acc[0] = d4{0, 0, 0, 0};
+            ++base[0];
+            rid = nrid;
+            nrid = ld_u32(a.cid[0] + base[0] + 1);
+          }
         }
+        if (valid) last_d = d;
+      };
+      // Two-stage software pipeline: the rows of the next leaf are in flight while this one
+      // is accumulated and its closes are handled (two register sets, no moves).
+      Leaf A = fetch(0), B;
+      for (uint32_t t = 0; t < nb; t += 2) {
+        B = fetch(t + 1);
+        consume(A, true);
+        A = fetch(t + 2);
+        consume(B, t + 1 < nb);
       }
       __syncwarp(gmask);  // every lane is done with this buffer before it is refilled
     }
