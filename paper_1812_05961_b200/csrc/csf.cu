@@ -95,9 +95,32 @@ struct FlagOut {
   int N;
 };
 
-__global__ void level_flags_kernel(FlagOut f, uint64_t nnz) {
+__device__ __forceinline__ uint32_t plan_code(const RootPlanRecOut& ro, uint64_t off, uint32_t id) {
+  const uint32_t s = ro.slotmap[off + id];  // (root2.cuh's row code: byte offset, bit 28 = hot)
+  return s != ~0u ? ((1u << 28) | (s * ro.ldb + ((s & 1u) << 4))) : id * ro.ldb;
+}
+
+// Also, with a ROOT plan under construction (ro.rec), leaf j's record: d = the first level
+// whose coordinate differs from leaf j+1 (the shallowest node ending at j; 0 at the last
+// leaf, N-1 if none), the codes of its leaf row and of the fiber closing here, its value.
+__global__ void level_flags_kernel(FlagOut f, uint64_t nnz, RootPlanRecOut ro) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
        j += (uint64_t)gridDim.x * blockDim.x) {
+    if (ro.rec) {
+      uint32_t dc = (uint32_t)(f.N - 1);
+      if (j + 1 == nnz) {
+        dc = 0;
+      } else {
+        for (int l = f.N - 2; l >= 0; --l)
+          if (f.c[l][j + 1] != f.c[l][j]) dc = (uint32_t)l;
+      }
+      const uint32_t code = plan_code(ro, ro.off_leaf, f.c[f.N - 1][j]);
+      const uint32_t fcode =
+          dc <= (uint32_t)(f.N - 2) ? plan_code(ro, ro.off_fiber, f.c[f.N - 2][j]) : 0u;
+      const double v = ro.vals[j];
+      ro.rec[j] = make_uint4(code | (dc << 29), fcode, (uint32_t)__double2loint(v),
+                             (uint32_t)__double2hiint(v));
+    }
     int d = f.N;  // first level whose coordinate differs from position j-1
     if (j == 0) {
       d = 0;
@@ -389,7 +412,13 @@ void finish_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& 
   fo.N = N;
   for (int l = 0; l < N; ++l) fo.c[l] = t.coord[l].p;
   for (int l = 0; l < N - 1; ++l) { node[l].alloc(nnz, st); fo.node[l] = node[l].p; }
-  level_flags_kernel<<<grid, 256, 0, st>>>(fo, nnz);
+  RootPlanRecOut ro;
+  bool plan = false;
+  if (ctx->build_plan_ld > 0) {
+    ArenaScope o(out_arena, false);  // the plan lives as long as the tree
+    plan = root_plan_begin(ctx, out, fo.c, t.vals.p, ctx->build_plan_ld, &ro);
+  }
+  level_flags_kernel<<<grid, 256, 0, st>>>(fo, nnz, ro);
   SB_CHECK_LAUNCH(ctx);
   size_t temp_bytes = 0;
   SB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, node[0].p, node[0].p, (int)nnz, st));
@@ -416,13 +445,9 @@ void finish_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& 
     SB_CHECK_LAUNCH(ctx);
   }
   tr.mark("scatter");
-  if (ctx->build_plan_ld > 0) {
-    const uint32_t* cp[SPLATT_MAX_NMODES];
-    const uint32_t* np[SPLATT_MAX_NMODES];
-    for (int l = 0; l < N; ++l) cp[l] = t.coord[l].p;
-    for (int l = 0; l < N - 1; ++l) np[l] = node[l].p;
-    ArenaScope o(out_arena, false);  // the plan lives as long as the tree
-    root_plan_from_levels(ctx, out, cp, np, t.vals.p, ctx->build_plan_ld);
+  if (plan) {
+    ArenaScope o(out_arena, false);
+    root_plan_end(ctx, out);
     tr.mark("root plan");
   }
   out.ids[N - 1] = std::move(t.coord[N - 1]);

@@ -22,6 +22,19 @@ struct RootPlan {
   DevBuf<uint4> rec;
   DevBuf<uint32_t> cid[SPLATT_MAX_NMODES];
   DevBuf<uint32_t> hot;
+  // while the builder forms the plan (root_plan_begin .. root_plan_end): (level, id) -> slot
+  DevBuf<uint32_t> slotmap;
+  uint64_t off[SPLATT_MAX_NMODES + 1] = {0};
+  bool ready = false;
+};
+
+// What the builder's level-flag kernel writes per leaf for a plan under construction.
+struct RootPlanRecOut {
+  uint4* rec = nullptr;        // nullptr: no plan
+  const uint32_t* slotmap = nullptr;
+  uint64_t off_leaf = 0, off_fiber = 0;  // slotmap offsets of levels N-1 and N-2
+  uint32_t ldb = 0;                      // row bytes (ld * 8)
+  const double* vals = nullptr;          // the tree's sorted values
 };
 
 // One CSF tree.  Level l < N-1: ids[l] (nodes[l]) and ptr[l] (nodes[l]+1, offsets into
@@ -98,12 +111,14 @@ void build_csf_set(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* 
                    uint64_t nnz, int N, const uint64_t* dims, const int* roots, int ntrees,
                    DevCsf* const* outs);
 
-// Second-generation ROOT plan of tree `out` for padded rank `ld`, from the builder's
-// level-order sorted coordinates coord[l][k] and inclusive node numbering node[l][k]
-// (1 + index of the level-l node containing leaf k, l < N-1) and the sorted values: no
-// walk over the tree's ptr arrays (root2.cu).  No-op unless root2 applies to `out`.
-void root_plan_from_levels(splatt_ctx* ctx, DevCsf& out, const uint32_t* const* coord,
-                           const uint32_t* const* node, const double* vals, int ld);
+// Second-generation ROOT plan of tree `out` for padded rank `ld`, formed by the builder
+// (root2.cu): root_plan_begin (before the level flags; returns false if root2 does not apply)
+// selects the hot rows from a sample of the level-order sorted coordinates and fills `ro`,
+// with which the flag kernel writes every leaf's record; root_plan_end (after the level
+// scatter) writes the coded node-id arrays from the tree's ids.  Both from the current arena.
+bool root_plan_begin(splatt_ctx* ctx, DevCsf& out, const uint32_t* const* coord,
+                     const double* vals, int ld, RootPlanRecOut* ro);
+void root_plan_end(splatt_ctx* ctx, DevCsf& out);
 
 // Ensure the chunk table for `chunk` leaves per work unit exists.
 void ensure_chunk_table(splatt_ctx* ctx, DevCsf& c, int chunk);

@@ -264,7 +264,7 @@ void mttkrp_level(splatt_ctx* ctx, DevCsf& c, int level, const double* const* fa
   auto launch = [&](DevCsf& t, int accumulate) {
     accumulate |= l1a;
     const int chunk = (int)t.tab_chunk;  // the tree's chunk table (mttkrp_prepare)
-    if (level == 0 && t.plan && t.plan->ld == ld && root2_eligible(ctx, t, ld)) {
+    if (level == 0 && t.plan && t.plan->ld == ld && t.plan->ready && root2_eligible(ctx, t, ld)) {
       mttkrp_root2_launch(ctx, t, fac_by_mode, out, ld, R, accumulate & 1);
       return;
     }

@@ -117,53 +117,28 @@ __global__ void code_level_kernel(const uint32_t* __restrict__ ids, uint64_t n,
     out[j] = code_of(slotmap, off, ids[j], ldb);
 }
 
-struct LevelArrays {
-  const uint32_t* coord[SPLATT_MAX_NMODES];  // level-order sorted coordinates (nnz each)
-  const uint32_t* node[SPLATT_MAX_NMODES];   // inclusive node numbering, levels 0..N-2
+struct CoordSet {
+  const uint32_t* c[SPLATT_MAX_NMODES];  // level-order sorted coordinates (nnz each)
   int N;
 };
 
-__device__ __forceinline__ bool node_starts(const LevelArrays& la, int l, uint64_t k) {
-  return k == 0 || la.node[l][k] != la.node[l][k - 1];
-}
-
 // Every kSample-th leaf: its id, and the id of every internal node (levels 1..N-2) that
-// starts there (each node has one start, so nodes are sampled at the same 1/kSample rate).
-__global__ void sampled_hist_levels_kernel(LevelArrays la, uint64_t nnz, LevelOffsets lo,
+// starts there — a level-l node starts at j when a coordinate of levels 0..l differs from
+// leaf j-1 (each node has one start, so nodes are sampled at the same 1/kSample rate).
+__global__ void sampled_hist_coords_kernel(CoordSet cs, uint64_t nnz, LevelOffsets lo,
                                            uint32_t* __restrict__ cnt) {
-  const int N = la.N;
+  const int N = cs.N;
   for (uint64_t k = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * kSample; k < nnz;
        k += (uint64_t)gridDim.x * blockDim.x * kSample) {
-    atomicAdd(&cnt[lo.off[N - 1] + la.coord[N - 1][k]], 1u);
+    atomicAdd(&cnt[lo.off[N - 1] + cs.c[N - 1][k]], 1u);
+    int ds = 0;  // first level whose coordinate differs from leaf k-1
+    if (k > 0) {
+      ds = N - 1;
+      for (int l = N - 2; l >= 0; --l)
+        if (cs.c[l][k] != cs.c[l][k - 1]) ds = l;
+    }
     for (int l = 1; l <= N - 2; ++l)
-      if (node_starts(la, l, k)) atomicAdd(&cnt[lo.off[l] + la.coord[l][k]], 1u);
-  }
-}
-
-// Records and coded node ids in one pass over the leaves: d = the shallowest level whose
-// node ends at leaf k (node numbering changes at k+1, or k is the last leaf); a level-l node
-// (l <= N-3) that starts at k writes its id (level 0) or code into cid[l].
-struct CidOut { uint32_t* cid[SPLATT_MAX_NMODES]; };
-__global__ void records_from_levels_kernel(LevelArrays la, const double* __restrict__ vals,
-                                           uint64_t nnz, const uint32_t* __restrict__ slotmap,
-                                           LevelOffsets lo, uint32_t ldb, CidOut co,
-                                           uint4* __restrict__ rec) {
-  const int N = la.N;
-  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nnz;
-       k += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t d = (uint32_t)(N - 1);
-    for (int l = N - 2; l >= 0; --l)
-      if (k + 1 == nnz || la.node[l][k + 1] != la.node[l][k]) d = (uint32_t)l;
-    const uint32_t code = code_of(slotmap, lo.off[N - 1], la.coord[N - 1][k], ldb);
-    const uint32_t fcode =
-        d <= (uint32_t)(N - 2) ? code_of(slotmap, lo.off[N - 2], la.coord[N - 2][k], ldb) : 0u;
-    const double v = vals[k];
-    rec[k] = make_uint4(code | (d << r2::kDShift), fcode, (uint32_t)__double2loint(v),
-                        (uint32_t)__double2hiint(v));
-    for (int l = 0; l <= N - 3; ++l)
-      if (node_starts(la, l, k))
-        co.cid[l][la.node[l][k] - 1] =
-            l == 0 ? la.coord[0][k] : code_of(slotmap, lo.off[l], la.coord[l][k], ldb);
+      if (ds <= l) atomicAdd(&cnt[lo.off[l] + cs.c[l][k]], 1u);
   }
 }
 
@@ -214,7 +189,7 @@ bool root2_eligible(const splatt_ctx* ctx, const DevCsf& c, int ld) {
 }
 
 void ensure_root_plan(splatt_ctx* ctx, DevCsf& c, int ld) {
-  if (c.plan && c.plan->ld == ld) return;
+  if (c.plan && c.plan->ld == ld && c.plan->ready) return;
   cudaStream_t st = ctx->stream;
   const int N = c.N;
   ArenaScope own(c.arena, false);  // lives as long as the tree
@@ -282,44 +257,41 @@ void ensure_root_plan(splatt_ctx* ctx, DevCsf& c, int ld) {
       SB_CHECK_LAUNCH(ctx);
     }
   }
+  plan->ready = true;
   c.plan = std::move(plan);
 }
 
-void root_plan_from_levels(splatt_ctx* ctx, DevCsf& c, const uint32_t* const* coord,
-                           const uint32_t* const* node, const double* vals, int ld) {
-  if (c.nnz == 0 || !root2_eligible(ctx, c, ld)) return;
+bool root_plan_begin(splatt_ctx* ctx, DevCsf& c, const uint32_t* const* coord,
+                     const double* vals, int ld, RootPlanRecOut* ro) {
+  if (c.nnz == 0 || !root2_eligible(ctx, c, ld)) return false;
   cudaStream_t st = ctx->stream;
   const int N = c.N;
   auto plan = std::make_unique<RootPlan>();  // from the current arena (the tree's)
   plan->ld = ld;
   plan->K = root2_hot_capacity(N, ld);
   if (const char* e = getenv("SPLATT_ROOT2_HOT")) plan->K = std::min<uint32_t>(plan->K, atoi(e));
-  const uint32_t ldb = (uint32_t)ld * 8u;
   LevelOffsets lo{};
   lo.N = N;
   uint64_t total = 0;
   for (int l = 1; l < N; ++l) { lo.off[l] = total; total += c.dims[l]; }
   lo.off[N] = total;
+  for (int l = 0; l <= N; ++l) plan->off[l] = lo.off[l];
   plan->rec.alloc(c.nnz, st);
-  CidOut co{};
-  for (int l = 0; l <= N - 3; ++l) {
-    plan->cid[l].alloc(c.nodes[l] + 1, st);
-    SB_CUDA(cudaMemsetAsync(plan->cid[l].p + c.nodes[l], 0, 4, st));
-    co.cid[l] = plan->cid[l].p;
-  }
   plan->hot.alloc(std::max<uint32_t>(1, plan->K), st);
-  LevelArrays la{};
-  la.N = N;
-  for (int l = 0; l < N; ++l) la.coord[l] = coord[l];
-  for (int l = 0; l < N - 1; ++l) la.node[l] = node[l];
+  {
+    ArenaScope pooled(nullptr, false);  // released by root_plan_end, not with the arena
+    plan->slotmap.alloc(total, st);
+  }
+  SB_CUDA(cudaMemsetAsync(plan->slotmap.p, 0xff, total * 4, st));
+  CoordSet cs{};
+  cs.N = N;
+  for (int l = 0; l < N; ++l) cs.c[l] = coord[l];
   {
     ArenaScope tmp(current_arena(), true);
-    DevBuf<uint32_t> cnt(total, st), cnt2(total, st), gidx(total, st), gidx2(total, st),
-        slotmap(total, st);
+    DevBuf<uint32_t> cnt(total, st), cnt2(total, st), gidx(total, st), gidx2(total, st);
     SB_CUDA(cudaMemsetAsync(cnt.p, 0, total * 4, st));
-    SB_CUDA(cudaMemsetAsync(slotmap.p, 0xff, total * 4, st));
-    sampled_hist_levels_kernel<<<grid_n(ctx, ceil_div(c.nnz, kSample)), 256, 0, st>>>(
-        la, c.nnz, lo, cnt.p);
+    sampled_hist_coords_kernel<<<grid_n(ctx, ceil_div(c.nnz, kSample)), 256, 0, st>>>(
+        cs, c.nnz, lo, cnt.p);
     SB_CHECK_LAUNCH(ctx);
     iota_u32_kernel<<<grid_n(ctx, total), 256, 0, st>>>(gidx.p, total);
     SB_CHECK_LAUNCH(ctx);
@@ -331,14 +303,40 @@ void root_plan_from_levels(splatt_ctx* ctx, DevCsf& c, const uint32_t* const* co
                                                       (int)total, 0, 32, st));
     if (plan->K > 0) {
       hot_slots_kernel<<<(unsigned)ceil_div(plan->K, 256), 256, 0, st>>>(
-          cnt2.p, gidx2.p, total, plan->K, lo, plan->hot.p, slotmap.p);
+          cnt2.p, gidx2.p, total, plan->K, lo, plan->hot.p, plan->slotmap.p);
       SB_CHECK_LAUNCH(ctx);
     }
-    records_from_levels_kernel<<<grid_n(ctx, c.nnz), 256, 0, st>>>(la, vals, c.nnz, slotmap.p, lo,
-                                                                   ldb, co, plan->rec.p);
-    SB_CHECK_LAUNCH(ctx);
   }
+  ro->rec = plan->rec.p;
+  ro->slotmap = plan->slotmap.p;
+  ro->off_leaf = lo.off[N - 1];
+  ro->off_fiber = lo.off[N - 2];
+  ro->ldb = (uint32_t)ld * 8u;
+  ro->vals = vals;
   c.plan = std::move(plan);
+  return true;
+}
+
+void root_plan_end(splatt_ctx* ctx, DevCsf& c) {
+  RootPlan& p = *c.plan;
+  cudaStream_t st = ctx->stream;
+  const int N = c.N;
+  const uint32_t ldb = (uint32_t)p.ld * 8u;
+  // padded id arrays (one entry more: the kernel loads one node ahead without a bounds test)
+  for (int l = 0; l <= N - 3; ++l) {
+    p.cid[l].alloc(c.nodes[l] + 1, st);
+    SB_CUDA(cudaMemsetAsync(p.cid[l].p + c.nodes[l], 0, 4, st));
+    if (l == 0) {
+      SB_CUDA(cudaMemcpyAsync(p.cid[0].p, c.ids[0].p, c.nodes[0] * 4, cudaMemcpyDeviceToDevice, st));
+    } else {
+      code_level_kernel<<<grid_n(ctx, c.nodes[l]), 256, 0, st>>>(c.ids[l].p, c.nodes[l],
+                                                                  p.slotmap.p, p.off[l], ldb,
+                                                                  p.cid[l].p);
+      SB_CHECK_LAUNCH(ctx);
+    }
+  }
+  p.slotmap.release();
+  p.ready = true;
 }
 
 namespace {
@@ -415,7 +413,7 @@ void launch2_n(splatt_ctx* ctx, DevCsf& c, const double* const* f, double* out, 
 
 void mttkrp_root2_launch(splatt_ctx* ctx, DevCsf& c, const double* const* f, double* out, int ld,
                          int R, int acc) {
-  if (!c.plan || c.plan->ld != ld) fail(SPLATT_ERR_CUDA, "internal: ROOT plan missing");
+  if (!c.plan || c.plan->ld != ld || !c.plan->ready) fail(SPLATT_ERR_CUDA, "internal: ROOT plan missing");
   if (c.N == 3) return launch2_n<3>(ctx, c, f, out, ld, R, acc);
   if (c.N == 4) return launch2_n<4>(ctx, c, f, out, ld, R, acc);
   fail(SPLATT_ERR_UNSUPPORTED, "internal: ROOT kernel v2 for N = 3, 4 only");

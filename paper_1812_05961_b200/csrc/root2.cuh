@@ -131,6 +131,11 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(P) : "memory");
 }
 
+// Cold-row load: L1::no_allocate (the hot rows are in shared memory).  SB_ROOT2_COLD_LD
+// overrides it for A/B runs (e.g. L1-allocating "ld.global.nc.v4.f64").
+#ifndef SB_ROOT2_COLD_LD
+#define SB_ROOT2_COLD_LD "ld.global.nc.L1::no_allocate.v4.f64"
+#endif
 // Predicated row gather (no branch, one code path for the whole warp): a hot code reads the
 // lane's two 16-byte halves from shared memory (sa0, sa1: 32-bit shared addresses), a cold
 // one reads 32 bytes from global memory (gp); `en` = false loads nothing (outputs undefined).
@@ -143,7 +148,7 @@ __device__ __forceinline__ d4 gather_pred(bool en, bool hot, uint32_t sa0, uint3
       "setp.eq.and.b32 pc, %4, 0, pe;\n\t"
       "@ph ld.shared.v2.f64 {%0,%1}, [%5];\n\t"
       "@ph ld.shared.v2.f64 {%2,%3}, [%6];\n\t"
-      "@pc ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%8];\n\t}"
+      "@pc " SB_ROOT2_COLD_LD " {%0,%1,%2,%3}, [%8];\n\t}"
       : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
       : "r"((uint32_t)hot), "r"(sa0), "r"(sa1), "r"((uint32_t)en), "l"(gp));
   return r;
@@ -155,7 +160,7 @@ __device__ __forceinline__ d4 gather_on(bool hot, uint32_t sa0, uint32_t sa1, co
       "setp.ne.b32 ph, %4, 0;\n\t"
       "@ph ld.shared.v2.f64 {%0,%1}, [%5];\n\t"
       "@ph ld.shared.v2.f64 {%2,%3}, [%6];\n\t"
-      "@!ph ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%7];\n\t}"
+      "@!ph " SB_ROOT2_COLD_LD " {%0,%1,%2,%3}, [%7];\n\t}"
       : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
       : "r"((uint32_t)hot), "r"(sa0), "r"(sa1), "l"(gp));
   return r;

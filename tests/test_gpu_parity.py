@@ -431,3 +431,36 @@ def test_root2_four_mode_seams_and_tiles(sb, monkeypatch, chunk):
             assert rel_fro(M, ref) <= MTTKRP_TOL, (tiling, n)
         del csf
         c.close()
+
+
+@pytest.mark.parametrize("R", [1, 5, 12, 16, 33, 40, 64, 100, 128])
+def test_root2_four_mode_every_group_width(sb, ctx, R):
+    """4-mode ROOT kernel v2 at every lane-group width (G = 2, 4, 8, 10 packed, 16, 32) and the
+    batch sizes / hot-table capacities they imply, garbage in the factors' pad columns."""
+    t = tensors()[4]  # c5-shaped (Zipf 1.05 x 4)
+    F = oracle.init_factors(t.dims, R, 11)
+    ind, vals = dev_coo(t)
+    csf = sb.csf_build(ind, vals, t.dims, ctx=ctx)
+    fd = dev_factors(F, sb.padded_ld(R), pad_value=float("nan")) if sb.padded_ld(R) > R \
+        else dev_factors(F, sb.padded_ld(R))
+    for n in range(4):
+        M = sb.mttkrp(csf, n, fd, rank=R).cpu().numpy()
+        assert np.all(M[:, R:] == 0.0)
+        assert rel_fro(M[:, :R], oracle.mttkrp(t.dims, t.ind, t.vals, F, n)) <= MTTKRP_TOL, n
+
+
+def test_root2_prebuilt_csf_and_hot_table_off(sb, monkeypatch):
+    """cpd_als on a prebuilt 4-mode CSF (the plan is built lazily from the tree, not by the
+    builder) and with the hot-row table disabled (SPLATT_ROOT2_HOT=0: every gather cold), both
+    against the oracle."""
+    t = tensors()[4]
+    R = 16
+    ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=R, max_iters=3, seed=4)
+    ind, vals = dev_coo(t)
+    c = sb.Context(0)
+    csf = sb.csf_build(ind, vals, t.dims, ctx=c)
+    als_compare(sb.cpd_als_csf(csf, rank=R, max_iters=3, seed=4, out_device=False), ref)
+    del csf
+    monkeypatch.setenv("SPLATT_ROOT2_HOT", "0")
+    als_compare(sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=3, seed=4, ctx=sb.Context(0),
+                           out_device=False), ref)
