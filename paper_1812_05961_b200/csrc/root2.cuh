@@ -172,6 +172,31 @@ __device__ __forceinline__ uint4 lds_u4(uint32_t sa) {
   return r;
 }
 
+// Record batches moved by the TMA engine (one cp.async.bulk per batch and group, completion on
+// an mbarrier; SB_ROOT2_TMA=1) or by per-lane 16-byte cp.async (0).
+#ifndef SB_ROOT2_TMA
+#define SB_ROOT2_TMA 1
+#endif
+__device__ __forceinline__ void mbar_init(uint32_t mb) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+}
+__device__ __forceinline__ void bulk_batch(uint32_t dst, const void* src, uint32_t bytes,
+                                           uint32_t mb) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the generic reads
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(mb) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W%=;\n\t}" ::"r"(mb), "r"(parity) : "memory");
+}
+
 template <int G, int T>
 struct Lanes {
   static constexpr int kPerWarp = 32 / G;
@@ -193,7 +218,8 @@ __host__ __device__ constexpr int batch_leaves() {
 }
 template <int G, int T>
 __host__ __device__ constexpr int rec_smem_bytes() {
-  return Lanes<G, T>::kGroups * group_rec_bytes(batch_leaves<G, T>());
+  // + two 8-byte mbarriers per group (TMA record batches), after all groups' tables
+  return Lanes<G, T>::kGroups * (group_rec_bytes(batch_leaves<G, T>()) + (SB_ROOT2_TMA ? 16 : 0));
 }
 template <int G, int T>
 inline uint32_t hot_capacity(int ld) {
@@ -239,6 +265,17 @@ __global__ void __launch_bounds__(Threads<N>::k, 1) mttkrp_root2_kernel(const Ar
   unsigned char* recbase = smem2 + (size_t)a.K * ld * 8 + (size_t)gib * kGroupRecBytes;
   uint4* buf0 = reinterpret_cast<uint4*>(recbase);
   const uint32_t rec_sa = (uint32_t)__cvta_generic_to_shared(recbase);
+#if SB_ROOT2_TMA
+  const uint32_t mbar_sa = (uint32_t)__cvta_generic_to_shared(
+      smem2 + (size_t)a.K * ld * 8 + (size_t)L::kGroups * kGroupRecBytes + (size_t)gib * 16);
+  if (q == 0) {
+    mbar_init(mbar_sa);
+    mbar_init(mbar_sa + 8);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp(gmask);
+  uint32_t phase = 0;  // bit w: parity of the next completion of buffer w's mbarrier
+#endif
   const bool active = 4u * q < ld;
   const uint32_t col = 4u * q;
   const uint32_t colc = active ? col : 0u;
@@ -267,9 +304,14 @@ __global__ void __launch_bounds__(Threads<N>::k, 1) mttkrp_root2_kernel(const Ar
     return __shfl_sync(gmask, v, gw * G);
   };
   auto issue_batch = [&](uint32_t kb, uint32_t nb, int which) {
+#if SB_ROOT2_TMA
+    if (q == 0) bulk_batch(rec_sa + (uint32_t)which * (kB * 16u), a.rec + kb, nb * 16u,
+                           mbar_sa + 8u * (uint32_t)which);
+#else
     uint4* dst = buf0 + which * kB;
     for (uint32_t j = q; j < nb; j += G) cp_async16(dst + j, a.rec + kb + j);
     cp_async_commit();
+#endif
   };
 
   constexpr int NM = (N > 3) ? (N - 3) : 1;  // levels 1..N-3 with a register-held open row
@@ -302,6 +344,11 @@ __global__ void __launch_bounds__(Threads<N>::k, 1) mttkrp_root2_kernel(const Ar
     int which = 0;
     for (uint32_t kb = k0; kb < k1; kb += kB, which ^= 1) {
       const uint32_t nb = min((uint32_t)kB, k1 - kb);
+#if SB_ROOT2_TMA
+      if (kb + kB < k1) issue_batch(kb + kB, min((uint32_t)kB, k1 - kb - kB), which ^ 1);
+      mbar_wait(mbar_sa + 8u * (uint32_t)which, (phase >> which) & 1u);
+      phase ^= 1u << which;
+#else
       if (kb + kB < k1) {
         issue_batch(kb + kB, min((uint32_t)kB, k1 - kb - kB), which ^ 1);
         cp_async_wait<1>();
@@ -309,6 +356,7 @@ __global__ void __launch_bounds__(Threads<N>::k, 1) mttkrp_root2_kernel(const Ar
         cp_async_wait<0>();
       }
       __syncwarp(gmask);
+#endif
       const uint32_t rb_sa = rec_sa + (uint32_t)which * (kB * 16u);
       // One leaf: its record (shared memory) and gathered rows.  Past the batch end the
       // last record is re-read and made inert (v = 0, no close, no gathers).
