@@ -241,13 +241,15 @@ void mttkrp_prepare(splatt_ctx* ctx, DevCsf& c, int level, int ld) {
     const int T = leaf_tiles(ctx, c, ld);
     if (T > 1 && c.tiles.empty()) tile_tree(ctx, c, T);
     for (auto& t : c.tiles) {
-      ensure_chunk_table(ctx, *t, mttkrp_chunk_leaves(*t));
-      if (t->nnz && root2_eligible(ctx, *t, ld)) ensure_root_plan(ctx, *t, ld);
+      const bool v2 = t->nnz && root2_eligible(ctx, *t, ld);
+      ensure_chunk_table(ctx, *t, v2 ? root2_table_chunk() : mttkrp_chunk_leaves(*t));
+      if (v2) ensure_root_plan(ctx, *t, ld);
     }
     if (!c.tiles.empty()) return;
   }
-  ensure_chunk_table(ctx, c, mttkrp_chunk_leaves(c));
-  if (level == 0 && root2_eligible(ctx, c, ld)) ensure_root_plan(ctx, c, ld);
+  const bool v2 = level == 0 && root2_eligible(ctx, c, ld);
+  ensure_chunk_table(ctx, c, v2 ? root2_table_chunk() : mttkrp_chunk_leaves(c));
+  if (v2) ensure_root_plan(ctx, c, ld);
   if (level > 0) ensure_hot(ctx, c, level);
 }
 

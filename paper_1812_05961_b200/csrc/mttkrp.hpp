@@ -39,6 +39,7 @@ double mttkrp_min_bytes(const DevCsf& c, int R, int level, const uint64_t* disti
 // its launch (acc bit 0: add into the owned rows).
 bool root2_eligible(const splatt_ctx* ctx, const DevCsf& c, int ld);
 void ensure_root_plan(splatt_ctx* ctx, DevCsf& c, int ld);
+int root2_table_chunk();  // leaves per chunk-table entry of a tree the kernel runs
 void mttkrp_root2_launch(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode,
                          double* out, int ld, int R, int acc);
 

@@ -18,7 +18,25 @@
 #include "mttkrp.hpp"
 #include "root2.cuh"
 
+#ifndef SB_ROOT2_TABLE
+#define SB_ROOT2_TABLE 256  // leaves per chunk-table entry of a tree run by this kernel
+#endif
+#ifndef SB_ROOT2_UNIT
+#define SB_ROOT2_UNIT 6  // table chunks per big work unit (6 x 256 = 1536 leaves)
+#endif
+#ifndef SB_ROOT2_TAIL
+#define SB_ROOT2_TAIL 2  // table chunks per group handed out one by one at the end
+#endif
+
 namespace sb {
+
+int root2_table_chunk() {
+  if (const char* e = getenv("SPLATT_CHUNK")) {
+    const int v = atoi(e);
+    if (v >= 32 && v % 32 == 0) return v;
+  }
+  return SB_ROOT2_TABLE;
+}
 
 namespace {
 
@@ -370,7 +388,16 @@ void launch2_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, dou
   // (the opt-in is cached per kernel and device: always ask for the whole budget)
   set_max_dynamic_smem((const void*)kern, r2::kSmemBudget);
   const uint64_t groups = (uint64_t)r2::Lanes<G, T>::kGroups;
-  uint64_t blocks = ceil_div(c.nchunks, groups);
+  // guided units (Args::unit): big units of kRoot2Unit table chunks while more than
+  // kRoot2Tail table chunks per group of the whole grid remain
+  {
+    const uint64_t all_groups = (uint64_t)ctx->num_sms * groups;
+    const uint64_t small = std::min<uint64_t>(c.nchunks, (uint64_t)SB_ROOT2_TAIL * all_groups);
+    a.unit = SB_ROOT2_UNIT;
+    a.nbig = (uint32_t)((c.nchunks - small) / SB_ROOT2_UNIT);
+    a.nunits = (uint32_t)(a.nbig + c.nchunks - (uint64_t)a.nbig * SB_ROOT2_UNIT);
+  }
+  uint64_t blocks = ceil_div(a.nunits, groups);
   if (blocks > (uint64_t)ctx->num_sms) {
     blocks = (uint64_t)ctx->num_sms;  // one CTA per SM, chunks taken dynamically
     ArenaScope own(c.arena, false);
@@ -385,7 +412,7 @@ void launch2_t(splatt_ctx* ctx, DevCsf& c, const double* const* fac_by_mode, dou
     }
     a.work = c.work.p;
     a.work_base = c.work_base;
-    c.work_base += (unsigned)(c.nchunks + blocks * groups);
+    c.work_base += (unsigned)(a.nunits + blocks * groups);
   }
   kern<<<(unsigned)blocks, T, smem, ctx->stream>>>(a);
   SB_CHECK_LAUNCH(ctx);

@@ -72,6 +72,10 @@ struct Args {
   const uint32_t* hot;              // K entries: (level << 28) | id, ~0u = empty slot
   uint32_t K;
   uint32_t nnz, nchunks, chunk, ld;
+  // Guided work units over the chunk table: units 0..nbig-1 take `unit` consecutive table
+  // chunks each, the rest one chunk each (the last few percent of the leaves go out in small
+  // pieces, so groups finish together); nunits = nbig + nchunks - nbig * unit.
+  uint32_t unit, nbig, nunits;
   int R;
   int accumulate;                   // add into the owned rows (later leaf tiles)
   const int* conv;
@@ -315,9 +319,11 @@ __global__ void __launch_bounds__(Threads<N>::k, 1) mttkrp_root2_kernel(const Ar
   };
 
   constexpr int NM = (N > 3) ? (N - 3) : 1;  // levels 1..N-3 with a register-held open row
-  for (uint32_t c = next_chunk(0, true); c < a.nchunks; c = next_chunk(c, false)) {
+  for (uint32_t u = next_chunk(0, true); u < a.nunits; u = next_chunk(u, false)) {
+    const uint32_t c = u < a.nbig ? u * a.unit : a.nbig * a.unit + (u - a.nbig);
+    const uint32_t cn = u < a.nbig ? a.unit : 1u;
     const uint32_t k0 = c * a.chunk;
-    const uint32_t k1 = min(k0 + a.chunk, a.nnz);
+    const uint32_t k1 = min(k0 + cn * a.chunk, a.nnz);
     uint32_t base[N - 1];
 #pragma unroll
     for (int l = 0; l < N - 1; ++l) base[l] = a.tab[(size_t)c * N + l];
