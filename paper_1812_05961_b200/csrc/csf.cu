@@ -133,20 +133,30 @@ __global__ void level_flags_kernel(FlagOut f, uint64_t nnz, RootPlanRecOut ro) {
 }
 
 // After the inclusive scans node[l][j] = 1 + index of the level-l node containing j.
-__global__ void scatter_level_kernel(uint64_t nnz, const uint32_t* __restrict__ node_l,
-                                     const uint32_t* __restrict__ node_child,  // null: leaves
-                                     const uint32_t* __restrict__ c_l, uint32_t* __restrict__ ids,
-                                     uint32_t* __restrict__ ptr, uint64_t n_nodes,
-                                     uint64_t n_children) {
+// All internal levels in one pass (each node array is read once, instead of once as the
+// level's and once as its parent's child numbering).
+struct LevelScatter {
+  const uint32_t* node[SPLATT_MAX_NMODES];  // levels 0..N-2
+  const uint32_t* c[SPLATT_MAX_NMODES];
+  uint32_t* ids[SPLATT_MAX_NMODES];
+  uint32_t* ptr[SPLATT_MAX_NMODES];
+  uint64_t nodes[SPLATT_MAX_NMODES];        // levels 0..N-1 (N-1: nnz)
+  int N;
+};
+__global__ void scatter_levels_kernel(LevelScatter ls, uint64_t nnz) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
        j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = node_l[j];
-    const bool start = (j == 0) || (node_l[j - 1] != k);
-    if (start) {
-      ids[k - 1] = c_l[j];
-      ptr[k - 1] = node_child ? node_child[j] - 1 : (uint32_t)j;
+    uint32_t child = (uint32_t)j + 1u;  // 1-based index of leaf j's node one level down
+    for (int l = ls.N - 2; l >= 0; --l) {
+      const uint32_t k = ls.node[l][j];
+      const bool start = (j == 0) || (ls.node[l][j - 1] != k);
+      if (!start) break;  // a node starting at j starts at every deeper level too
+      ls.ids[l][k - 1] = ls.c[l][j];
+      ls.ptr[l][k - 1] = child - 1u;
+      child = k;
     }
-    if (j == 0) ptr[n_nodes] = (uint32_t)n_children;
+    if (j == 0)
+      for (int l = 0; l < ls.N - 1; ++l) ls.ptr[l][ls.nodes[l]] = (uint32_t)ls.nodes[l + 1];
   }
 }
 
@@ -432,18 +442,22 @@ void finish_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& 
   host_sync(ctx);
   for (int l = 0; l < N - 1; ++l) out.nodes[l] = counts[l];
   out.nodes[N - 1] = nnz;
+  LevelScatter ls{};
+  ls.N = N;
   for (int l = 0; l < N - 1; ++l) {
     {
       ArenaScope o(out_arena, false);
       out.ids[l].alloc(out.nodes[l], st);
       out.ptr[l].alloc(out.nodes[l] + 1, st);
     }
-    const uint32_t* child = (l == N - 2) ? nullptr : node[l + 1].p;
-    scatter_level_kernel<<<grid, 256, 0, st>>>(nnz, node[l].p, child, t.coord[l].p,
-                                               out.ids[l].p, out.ptr[l].p, out.nodes[l],
-                                               out.nodes[l + 1]);
-    SB_CHECK_LAUNCH(ctx);
+    ls.node[l] = node[l].p;
+    ls.c[l] = t.coord[l].p;
+    ls.ids[l] = out.ids[l].p;
+    ls.ptr[l] = out.ptr[l].p;
   }
+  for (int l = 0; l < N; ++l) ls.nodes[l] = out.nodes[l];
+  scatter_levels_kernel<<<grid, 256, 0, st>>>(ls, nnz);
+  SB_CHECK_LAUNCH(ctx);
   tr.mark("scatter");
   if (plan) {
     ArenaScope o(out_arena, false);
