@@ -313,6 +313,57 @@ __global__ void gather_levels_kernel(CoordOut co, uint64_t nnz, const uint32_t* 
   }
 }
 
+constexpr uint64_t kBlockLeaves = 8;  // mean leaves per node for the block move
+// Derived tree rooted at Q's level j (1 <= j <= N-2), by blocks: the Q-ordered leaves of one
+// level-j node stay together and in order, so a stable sort of the leaves by the level-j
+// coordinate is a stable sort of the F_j level-j NODES by that coordinate, followed by a
+// block move of their leaves (F_j << nnz: c5's mode-2 tree sorts 4M keys instead of 150M).
+__global__ void node_keys_kernel(const uint32_t* __restrict__ node_j,
+                                 const uint32_t* __restrict__ coord_j, uint64_t nnz,
+                                 uint32_t* __restrict__ key, uint32_t* __restrict__ start,
+                                 uint32_t* __restrict__ idx) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t n1 = node_j[k];
+    if (k == 0 || node_j[k - 1] != n1) {
+      key[n1 - 1] = coord_j[k];
+      start[n1 - 1] = (uint32_t)k;
+      idx[n1 - 1] = n1 - 1;
+    }
+  }
+}
+// leaves of the i-th node in sorted order
+__global__ void node_sizes_kernel(const uint32_t* __restrict__ sidx,
+                                  const uint32_t* __restrict__ start, uint64_t F, uint64_t nnz,
+                                  uint32_t* __restrict__ sz) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < F;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t n = sidx[i];
+    sz[i] = (n + 1 < F ? start[n + 1] : (uint32_t)nnz) - start[n];
+  }
+}
+__global__ void node_newstart_kernel(const uint32_t* __restrict__ sidx,
+                                     const uint32_t* __restrict__ off, uint64_t F,
+                                     uint32_t* __restrict__ newstart) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < F;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    newstart[sidx[i]] = off[i];
+}
+// leaf k (Q order) -> its position in the derived order; the derived tree's root coordinate
+__global__ void node_dest_kernel(const uint32_t* __restrict__ node_j,
+                                 const uint32_t* __restrict__ coord_j,
+                                 const uint32_t* __restrict__ start,
+                                 const uint32_t* __restrict__ newstart, uint64_t nnz,
+                                 uint32_t* __restrict__ perm, uint32_t* __restrict__ root) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t n = node_j[k] - 1u;
+    const uint32_t d = newstart[n] + ((uint32_t)k - start[n]);
+    perm[d] = (uint32_t)k;
+    root[d] = coord_j[k];
+  }
+}
+
 // Full sort of the COO into the order of `perm`: packed composite keys (one or more <= 64-bit
 // groups, LSD), stable radix sort of (key, position), then decode / gather into t (allocated
 // by the caller, alloc_sorted).
@@ -412,36 +463,57 @@ void alloc_sorted(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, Arena* ou
 // Levels of a tree from its sorted coordinates: "prefix 0..l changed" flags, inclusive scans
 // numbering the nodes, one host sync for the node counts, scatter of ids/ptr.  Moves
 // t.coord[N-1] and t.vals into the tree.
-void finish_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& out,
-                   Arena* out_arena, PhaseTrace& tr) {
+// A tree's node numbering: node[l][j] = 1 + index of the level-l node containing sorted
+// position j (inclusive scans of "prefix 0..l changed" flags), and the node counts.
+struct LevelNumbering {
+  DevBuf<uint32_t> node[SPLATT_MAX_NMODES];
+  uint64_t counts[SPLATT_MAX_NMODES] = {0};
+  bool plan = false;  // a ROOT plan is under construction (its records written by the flags)
+};
+
+// Flags (+ the ROOT plan's records), scans, one host sync for the node counts.  The node
+// arrays come from the current arena (the caller's scope).
+void number_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& out,
+                   Arena* out_arena, LevelNumbering& nb, PhaseTrace& tr) {
   cudaStream_t st = ctx->stream;
   const int grid = grid_for(ctx, nnz);
-  ArenaScope tmp_scope(current_arena(), true);
-  DevBuf<uint32_t> node[SPLATT_MAX_NMODES];
   FlagOut fo{};
   fo.N = N;
   for (int l = 0; l < N; ++l) fo.c[l] = t.coord[l].p;
-  for (int l = 0; l < N - 1; ++l) { node[l].alloc(nnz, st); fo.node[l] = node[l].p; }
+  for (int l = 0; l < N - 1; ++l) { nb.node[l].alloc(nnz, st); fo.node[l] = nb.node[l].p; }
   RootPlanRecOut ro;
-  bool plan = false;
   if (ctx->build_plan_ld > 0) {
     ArenaScope o(out_arena, false);  // the plan lives as long as the tree
-    plan = root_plan_begin(ctx, out, fo.c, t.vals.p, ctx->build_plan_ld, &ro);
+    nb.plan = root_plan_begin(ctx, out, fo.c, t.vals.p, ctx->build_plan_ld, &ro);
   }
   level_flags_kernel<<<grid, 256, 0, st>>>(fo, nnz, ro);
   SB_CHECK_LAUNCH(ctx);
-  size_t temp_bytes = 0;
-  SB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, node[0].p, node[0].p, (int)nnz, st));
-  DevBuf<uint8_t> temp(temp_bytes, st);
-  for (int l = 0; l < N - 1; ++l)
-    SB_CUDA(cub::DeviceScan::InclusiveSum(temp.p, temp_bytes, node[l].p, node[l].p, (int)nnz, st));
+  {
+    ArenaScope tmp_scope(current_arena(), true);
+    size_t temp_bytes = 0;
+    SB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, nb.node[0].p, nb.node[0].p,
+                                          (int)nnz, st));
+    DevBuf<uint8_t> temp(temp_bytes, st);
+    for (int l = 0; l < N - 1; ++l)
+      SB_CUDA(cub::DeviceScan::InclusiveSum(temp.p, temp_bytes, nb.node[l].p, nb.node[l].p,
+                                            (int)nnz, st));
+  }
   tr.mark("flags+scan");
   std::vector<uint32_t> counts(N, 0);
   for (int l = 0; l < N - 1; ++l)
-    SB_CUDA(cudaMemcpyAsync(&counts[l], node[l].p + (nnz - 1), 4, cudaMemcpyDeviceToHost, st));
+    SB_CUDA(cudaMemcpyAsync(&counts[l], nb.node[l].p + (nnz - 1), 4, cudaMemcpyDeviceToHost, st));
   host_sync(ctx);
-  for (int l = 0; l < N - 1; ++l) out.nodes[l] = counts[l];
-  out.nodes[N - 1] = nnz;
+  for (int l = 0; l < N - 1; ++l) nb.counts[l] = counts[l];
+  nb.counts[N - 1] = nnz;
+}
+
+// Scatter of ids/ptr, the ROOT plan's node-id arrays; moves t.coord[N-1] and t.vals into the
+// tree.
+void complete_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& out,
+                     Arena* out_arena, LevelNumbering& nb, PhaseTrace& tr) {
+  cudaStream_t st = ctx->stream;
+  const int grid = grid_for(ctx, nnz);
+  for (int l = 0; l < N; ++l) out.nodes[l] = nb.counts[l];
   LevelScatter ls{};
   ls.N = N;
   for (int l = 0; l < N - 1; ++l) {
@@ -450,7 +522,7 @@ void finish_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& 
       out.ids[l].alloc(out.nodes[l], st);
       out.ptr[l].alloc(out.nodes[l] + 1, st);
     }
-    ls.node[l] = node[l].p;
+    ls.node[l] = nb.node[l].p;
     ls.c[l] = t.coord[l].p;
     ls.ids[l] = out.ids[l].p;
     ls.ptr[l] = out.ptr[l].p;
@@ -459,7 +531,7 @@ void finish_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& 
   scatter_levels_kernel<<<grid, 256, 0, st>>>(ls, nnz);
   SB_CHECK_LAUNCH(ctx);
   tr.mark("scatter");
-  if (plan) {
+  if (nb.plan) {
     ArenaScope o(out_arena, false);
     root_plan_end(ctx, out);
     tr.mark("root plan");
@@ -469,6 +541,15 @@ void finish_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& 
   out.tab_chunk = 0;
   out.nchunks = 0;
   out.tab.release();
+}
+
+// Levels of a tree from its sorted coordinates (number_levels + complete_levels).
+void finish_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& out,
+                   Arena* out_arena, PhaseTrace& tr) {
+  ArenaScope tmp_scope(current_arena(), true);
+  LevelNumbering nb;
+  number_levels(ctx, t, nnz, N, out, out_arena, nb, tr);
+  complete_levels(ctx, t, nnz, N, out, out_arena, nb, tr);
 }
 
 // `arena`: the allocator the tree's arrays come from (nullptr: the stream-ordered pool); the
@@ -524,27 +605,67 @@ void build_csf_set(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* 
   if (ntrees > (qtree >= 0 ? 1 : 0) && total_bits <= 64) tq.kv.alloc(nnz, st);
   sort_full(ctx, d_ind, d_vals, nnz, N, dims, Q, tq, tr);
   const int grid = grid_for(ctx, nnz);
+  // The Q tree's node numbering first when a derived tree can be built by node blocks (its
+  // root at Q level 1..N-2); its scatter / plan completion comes last, as before.
+  bool blocks = false;
+  for (int k = 0; k < ntrees && qtree >= 0; ++k)
+    if (k != qtree && qlev[roots[k]] >= 1 && qlev[roots[k]] <= N - 2) blocks = true;
+  // (the numbering is needed anyway; only its node counts decide, per tree, below)
+  if (getenv("SPLATT_BUILD_NOBLOCKS")) blocks = false;  // A/B runs: leaf re-sorts only
+  LevelNumbering qn;
+  if (blocks) number_levels(ctx, tq, nnz, N, *outs[qtree], out_arena, qn, tr);
   for (int k = 0; k < ntrees; ++k) {
     if (k == qtree) continue;
     DevCsf& out = *outs[k];
     const int r = roots[k];
+    const int j = qlev[r];
     ArenaScope tree_scope(current_arena(), true);
     SortedTree tr_;
     alloc_sorted(ctx, tr_, nnz, N, out_arena, true);
     {
       ArenaScope sort_scope(current_arena(), true);
-      DevBuf<uint32_t> pos(nnz, st), perm_out(nnz, st);
-      iota_kernel<<<grid, 256, 0, st>>>(pos.p, nnz);
-      SB_CHECK_LAUNCH(ctx);
-      size_t temp_bytes = 0;
+      DevBuf<uint32_t> perm_out(nnz, st);
       const int nb = std::max(1, bits_for(dims[r]));
-      SB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, tq.coord[qlev[r]].p,
-                                              tr_.coord[0].p, pos.p, perm_out.p, (int)nnz, 0, nb,
-                                              st));
-      DevBuf<uint8_t> temp(temp_bytes, st);
-      SB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, tq.coord[qlev[r]].p,
-                                              tr_.coord[0].p, pos.p, perm_out.p, (int)nnz, 0, nb,
-                                              st));
+      // (blocks only where they are long: the block move scatters each node's leaves
+      // together, so ~2-leaf nodes would turn it into a random scatter — c5's mode-1 tree,
+      // 77M nodes: 11.8 ms against 5.0 for the leaf re-sort)
+      if (blocks && j >= 1 && j <= N - 2 && nnz >= kBlockLeaves * qn.counts[j]) {
+        const uint64_t F = qn.counts[j];
+        DevBuf<uint32_t> key(F, st), skey(F, st), idx(F, st), sidx(F, st), start(F, st),
+            sz(F, st), off(F, st), newstart(F, st);
+        node_keys_kernel<<<grid, 256, 0, st>>>(qn.node[j].p, tq.coord[j].p, nnz, key.p, start.p,
+                                               idx.p);
+        SB_CHECK_LAUNCH(ctx);
+        size_t tb = 0;
+        SB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, skey.p, idx.p, sidx.p, (int)F,
+                                                0, nb, st));
+        size_t tb2 = 0;
+        SB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, sz.p, off.p, (int)F, st));
+        DevBuf<uint8_t> temp(std::max(tb, tb2), st);
+        SB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb, key.p, skey.p, idx.p, sidx.p, (int)F,
+                                                0, nb, st));
+        const int gF = grid_for(ctx, F);
+        node_sizes_kernel<<<gF, 256, 0, st>>>(sidx.p, start.p, F, nnz, sz.p);
+        SB_CHECK_LAUNCH(ctx);
+        SB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb2, sz.p, off.p, (int)F, st));
+        node_newstart_kernel<<<gF, 256, 0, st>>>(sidx.p, off.p, F, newstart.p);
+        SB_CHECK_LAUNCH(ctx);
+        node_dest_kernel<<<grid, 256, 0, st>>>(qn.node[j].p, tq.coord[j].p, start.p, newstart.p,
+                                               nnz, perm_out.p, tr_.coord[0].p);
+        SB_CHECK_LAUNCH(ctx);
+      } else {
+        DevBuf<uint32_t> pos(nnz, st);
+        iota_kernel<<<grid, 256, 0, st>>>(pos.p, nnz);
+        SB_CHECK_LAUNCH(ctx);
+        size_t temp_bytes = 0;
+        SB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, tq.coord[j].p,
+                                                tr_.coord[0].p, pos.p, perm_out.p, (int)nnz, 0,
+                                                nb, st));
+        DevBuf<uint8_t> temp(temp_bytes, st);
+        SB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, tq.coord[j].p,
+                                                tr_.coord[0].p, pos.p, perm_out.p, (int)nnz, 0,
+                                                nb, st));
+      }
       if (tq.kv.p) {
         KvOut ko{};
         ko.N = N;
@@ -568,7 +689,10 @@ void build_csf_set(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* 
     }
     finish_levels(ctx, tr_, nnz, N, out, out_arena, tr);
   }
-  if (qtree >= 0) finish_levels(ctx, tq, nnz, N, *outs[qtree], out_arena, tr);
+  if (qtree >= 0) {
+    if (blocks) complete_levels(ctx, tq, nnz, N, *outs[qtree], out_arena, qn, tr);
+    else finish_levels(ctx, tq, nnz, N, *outs[qtree], out_arena, tr);
+  }
 }
 
 namespace {

@@ -48,7 +48,7 @@ inline int grid_n(splatt_ctx* ctx, uint64_t n) {
 }
 
 #ifndef SB_PLAN_SAMPLE
-#define SB_PLAN_SAMPLE 64
+#define SB_PLAN_SAMPLE 256
 #endif
 constexpr uint32_t kSample = SB_PLAN_SAMPLE;  // histogram: every kSample-th node / leaf
 
