@@ -33,22 +33,55 @@ __global__ void validate_kernel(IndSet s, uint64_t nnz, int* bad) {
   if (__any_sync(0xffffffffu, local) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
 }
 
-// Composite key of levels [lo, hi) (level order), most significant = lo.
+// Composite key of levels [lo, hi) (level order), most significant = lo: bit fields
+// (coordinate << shift[l]), or — `mixed`, one key group only — the mixed-radix number
+// sum_l c_l * stride[l] with stride[l] = prod_{m > l} I_m, whose ceil(log2 prod I) bits can
+// save a radix pass (c5: 57 -> 56 bits, 8 -> 7 passes).  Both orders are the lexicographic
+// order of the coordinates (c_l < I_l).
 struct KeySpec {
   const uint32_t* src[SPLATT_MAX_NMODES];  // per level (already in level order)
   int shift[SPLATT_MAX_NMODES];
+  uint64_t stride[SPLATT_MAX_NMODES];
   int lo, hi;
+  bool mixed;
 };
 
+// Mixed-radix digits of a key: c[l] = (k / stride[l]) mod I_l for l = N-1 down to 0, by
+// successive division (a double-precision quotient corrected to the exact one; k < 2^63).
+struct MixedRadix {
+  uint32_t dim[SPLATT_MAX_NMODES];
+  double inv[SPLATT_MAX_NMODES];  // 1 / dim
+  int N;
+};
+__device__ __forceinline__ void mixed_decode(const MixedRadix& mr, uint64_t k, uint32_t* c) {
+  for (int l = mr.N - 1; l >= 0; --l) {
+    const uint64_t d = mr.dim[l];
+    if (d == 1) { c[l] = 0; continue; }
+    uint64_t q = (uint64_t)((double)k * mr.inv[l]);
+    long long r = (long long)(k - q * d);
+    while (r < 0) { --q; r += (long long)d; }
+    while (r >= (long long)d) { ++q; r -= (long long)d; }
+    c[l] = (uint32_t)r;
+    k = q;
+  }
+}
+
+// Also (vbits != nullptr, first group only) the values' bits, carried through the sort.
 __global__ void pack_keys_kernel(KeySpec ks, uint64_t nnz, const uint32_t* __restrict__ order,
-                                 uint64_t* __restrict__ keys, uint32_t* __restrict__ pos) {
+                                 uint64_t* __restrict__ keys, uint32_t* __restrict__ pos,
+                                 const double* __restrict__ vin, uint64_t* __restrict__ vbits) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
        j += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t q = order ? order[j] : (uint32_t)j;
     uint64_t k = 0;
-    for (int l = ks.lo; l < ks.hi; ++l) k |= (uint64_t)ks.src[l][q] << ks.shift[l];
+    if (ks.mixed) {
+      for (int l = ks.lo; l < ks.hi; ++l) k += (uint64_t)ks.src[l][q] * ks.stride[l];
+    } else {
+      for (int l = ks.lo; l < ks.hi; ++l) k |= (uint64_t)ks.src[l][q] << ks.shift[l];
+    }
     keys[j] = k;
-    if (!order) pos[j] = (uint32_t)j;
+    if (vbits) vbits[j] = (uint64_t)__double_as_longlong(vin[j]);
+    else if (!order) pos[j] = (uint32_t)j;
   }
 }
 
@@ -71,18 +104,24 @@ __global__ void gather_kernel(CoordOut co, uint64_t nnz, const uint32_t* __restr
 struct BitSet { int b[SPLATT_MAX_NMODES]; };
 
 // coordinate of level l at sorted position j = bits of the sorted composite key.
-__global__ void decode_kernel(KeySpec ks, BitSet bs, CoordOut co, uint64_t nnz,
+__global__ void decode_kernel(KeySpec ks, BitSet bs, MixedRadix mr, CoordOut co, uint64_t nnz,
                               const uint64_t* __restrict__ keys, const uint32_t* __restrict__ P,
                               const double* __restrict__ vin, double* __restrict__ vout,
                               double2* __restrict__ kv) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nnz;
        j += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k = keys[j];
-    for (int l = 0; l < co.N; ++l) {
-      const uint64_t m = bs.b[l] >= 64 ? ~0ull : ((1ull << bs.b[l]) - 1ull);
-      co.dst[l][j] = (uint32_t)((k >> ks.shift[l]) & m);
+    if (ks.mixed) {
+      uint32_t c[SPLATT_MAX_NMODES];
+      mixed_decode(mr, k, c);
+      for (int l = 0; l < co.N; ++l) co.dst[l][j] = c[l];
+    } else {
+      for (int l = 0; l < co.N; ++l) {
+        const uint64_t m = bs.b[l] >= 64 ? ~0ull : ((1ull << bs.b[l]) - 1ull);
+        co.dst[l][j] = (uint32_t)((k >> ks.shift[l]) & m);
+      }
     }
-    const double v = vin[P[j]];
+    const double v = P ? vin[P[j]] : vin[j];  // (no P: the values travelled with the keys)
     vout[j] = v;
     if (kv) kv[j] = make_double2(__longlong_as_double((long long)k), v);
   }
@@ -129,6 +168,177 @@ __global__ void level_flags_kernel(FlagOut f, uint64_t nnz, RootPlanRecOut ro) {
         if (f.c[l][j] != f.c[l][j - 1]) d = l;
     }
     for (int l = 0; l < f.N - 1; ++l) f.node[l][j] = (d <= l) ? 1u : 0u;
+  }
+}
+
+// ---- Levels of a tree in two passes over its sorted coordinates, without node-number arrays
+// (the derived trees).  The leaves are split into contiguous ranges, one per
+// CTA of a persistent grid.  Pass 1 counts the node starts of every internal level in each
+// range; a small scan turns the counts into each range's first node index per level (and the
+// level totals, which size ids/ptr); pass 2 recomputes the starts, numbers them by a block
+// scan on top of the range's running index, and writes ids/ptr (and a ROOT plan's per-leaf
+// records) directly.
+constexpr int kLvThreads = 256, kLvPer = 4;                 // rows of 32 leaves per warp step
+constexpr int kLvTile = kLvThreads * kLvPer;                // leaves per CTA step in pass 2
+
+struct LevelIn {
+  const uint32_t* c[SPLATT_MAX_NMODES];  // sorted coordinates per level (nnz each)
+  int N;
+};
+
+// First level l <= N-2 whose coordinate at leaf j differs from leaf j-1 (0 at j = 0; N-1:
+// none, i.e. only a new leaf starts at j).
+template <int N>
+__device__ __forceinline__ int first_diff(const LevelIn& li, uint64_t j) {
+  if (j == 0) return 0;
+  int d = N - 1;
+#pragma unroll
+  for (int l = N - 2; l >= 0; --l)
+    if (__ldg(li.c[l] + j) != __ldg(li.c[l] + j - 1)) d = l;
+  return d;
+}
+
+// counts[r * (N-1) + l] = node starts of level l among the leaves of range r.
+template <int N>
+__global__ void __launch_bounds__(256) level_count_kernel(LevelIn li, uint64_t nnz, uint64_t range,
+                                                          uint32_t* __restrict__ counts) {
+  constexpr int L = N - 1;
+  __shared__ uint32_t sc[SPLATT_MAX_NMODES];
+  if (threadIdx.x < SPLATT_MAX_NMODES) sc[threadIdx.x] = 0u;
+  __syncthreads();
+  uint32_t cnt[SPLATT_MAX_NMODES] = {0};
+  const uint64_t lo = blockIdx.x * range, hi = min(nnz, lo + range);
+  for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+    const int d = first_diff<N>(li, j);
+#pragma unroll
+    for (int l = 0; l < L; ++l) cnt[l] += (d <= l) ? 1u : 0u;
+  }
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    uint32_t v = cnt[l];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&sc[l], v);
+  }
+  __syncthreads();
+  if (threadIdx.x < L) counts[(size_t)blockIdx.x * L + threadIdx.x] = sc[threadIdx.x];
+}
+
+// In place: counts[r][l] -> sum over ranges r' < r; totals[l] = the level's node count.
+__global__ void level_scan_kernel(uint32_t* __restrict__ counts, int nranges, int L,
+                                  uint32_t* __restrict__ totals) {
+  const int l = threadIdx.x;
+  if (l >= L) return;
+  uint32_t run = 0u;
+  for (int r = 0; r < nranges; ++r) {
+    const uint32_t v = counts[(size_t)r * L + l];
+    counts[(size_t)r * L + l] = run;
+    run += v;
+  }
+  totals[l] = run;
+}
+
+struct LevelOut {
+  uint32_t* ids[SPLATT_MAX_NMODES];
+  uint32_t* ptr[SPLATT_MAX_NMODES];
+};
+
+// Pass 2.  A step of the CTA covers kLvTile leaves, warp w the kLvPer rows of 32 consecutive
+// leaves at [step + 256 w, step + 256 (w + 1)): every load and store is a coalesced row.  A
+// leaf's node starts at level l are the ballot of (d <= l) over its row; its node index is the
+// range's running base + the starts of the lower warps (shared memory) + of the earlier rows
+// of its warp + of the lower lanes of its row (popc of the ballot).
+template <int N>
+__global__ void __launch_bounds__(kLvThreads) level_write_kernel(LevelIn li, uint64_t nnz,
+                                                                 uint64_t range,
+                                                                 const uint32_t* __restrict__ bases,
+                                                                 const uint32_t* __restrict__ totals,
+                                                                 LevelOut lo, RootPlanRecOut ro) {
+  constexpr int L = N - 1;
+  constexpr int kWarps = kLvThreads / 32;
+  __shared__ uint32_t s_cnt[kWarps][L];
+  __shared__ uint32_t s_base[L];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint64_t r0 = blockIdx.x * range, r1 = min(nnz, r0 + range);
+  if (threadIdx.x < L) s_base[threadIdx.x] = bases[(size_t)blockIdx.x * L + threadIdx.x];
+  uint32_t pend[L];  // last warp: the range's running bases after its step
+  for (uint64_t step = r0; step < r1; step += kLvTile) {
+    const uint64_t wb = step + (uint64_t)warp * 32u * kLvPer;
+    int d[kLvPer];
+    uint32_t ball[kLvPer][L];
+    uint32_t wcnt[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) wcnt[l] = 0u;
+#pragma unroll
+    for (int i = 0; i < kLvPer; ++i) {
+      const uint64_t j = wb + (uint64_t)i * 32u + lane;
+      d[i] = (j < r1) ? first_diff<N>(li, j) : N - 1;
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        ball[i][l] = __ballot_sync(0xffffffffu, d[i] <= l);
+        wcnt[l] += (uint32_t)__popc(ball[i][l]);
+      }
+    }
+    __syncthreads();  // s_cnt / s_base of the previous step consumed by every warp
+    if (lane < L) {
+#pragma unroll
+      for (int l = 0; l < L; ++l)
+        if (lane == l) {
+          s_cnt[warp][l] = wcnt[l];
+          if (warp == kWarps - 1 && step > r0) s_base[l] = pend[l];  // previous step's end
+        }
+    }
+    __syncthreads();
+    uint32_t next[L];  // index of this warp's next start per level (before its rows)
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      uint32_t off = s_base[l];
+      for (int x = 0; x < warp; ++x) off += s_cnt[x][l];
+      next[l] = off;
+    }
+#pragma unroll
+    for (int i = 0; i < kLvPer; ++i) {
+      const uint64_t j = wb + (uint64_t)i * 32u + lane;
+      const bool valid = j < r1;
+      uint32_t k[L];
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        k[l] = next[l] + (uint32_t)__popc(ball[i][l] & lt);
+        next[l] += (uint32_t)__popc(ball[i][l]);
+      }
+      if (valid) {
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          if (l >= d[i]) {
+            lo.ids[l][k[l]] = __ldg(li.c[l] + j);
+            lo.ptr[l][k[l]] = (l == L - 1) ? (uint32_t)j : k[l + 1 < L ? l + 1 : l];
+          }
+        }
+        if (ro.rec) {
+          // d of leaf j+1: the shallowest node ending at leaf j (0 at the last leaf)
+          int dn = __shfl_down_sync(0xffffffffu, d[i], 1);
+          if (lane == 31 || j + 1 >= r1) dn = (j + 1 < nnz) ? first_diff<N>(li, j + 1) : 0;
+          const uint32_t dc = (uint32_t)dn;
+          const uint32_t code = plan_code(ro, ro.off_leaf, __ldg(li.c[N - 1] + j));
+          const uint32_t fcode =
+              dc <= (uint32_t)(N - 2) ? plan_code(ro, ro.off_fiber, __ldg(li.c[N - 2] + j)) : 0u;
+          const double v = ro.vals[j];
+          ro.rec[j] = make_uint4(code | (dc << 29), fcode, (uint32_t)__double2loint(v),
+                                 (uint32_t)__double2hiint(v));
+        }
+        if (j + 1 == nnz) {
+#pragma unroll
+          for (int l = 0; l < L; ++l)
+            lo.ptr[l][totals[l]] = (l + 1 < L) ? totals[l + 1] : (uint32_t)nnz;
+        }
+      } else if (ro.rec) {
+        (void)__shfl_down_sync(0xffffffffu, d[i], 1);  // (every lane takes part)
+      }
+    }
+    // the last warp's final indices are the next step's bases (stored after the next barrier)
+#pragma unroll
+    for (int l = 0; l < L; ++l) pend[l] = next[l];
   }
 }
 
@@ -272,11 +482,16 @@ struct SortedTree {
   // N coordinates and a value (N + 1 random reads, each a DRAM burst).
   DevBuf<double2> kv;
   int shift[SPLATT_MAX_NMODES] = {0}, bits[SPLATT_MAX_NMODES] = {0};
+  bool mixed = false;  // kv keys are mixed-radix (KeySpec::mixed), decoded with `mr`
+  MixedRadix mr{};
 };
 
 struct KvOut {
   uint32_t* dst[SPLATT_MAX_NMODES];  // tree levels 1..N-1
   int shift[SPLATT_MAX_NMODES], bits[SPLATT_MAX_NMODES];
+  int qlev[SPLATT_MAX_NMODES];       // mixed keys: the Q level of each tree level
+  bool mixed;
+  MixedRadix mr;
   int N;
 };
 
@@ -288,9 +503,15 @@ __global__ void gather_kv_kernel(KvOut ko, uint64_t nnz, const uint32_t* __restr
        j += (uint64_t)gridDim.x * blockDim.x) {
     const double2 r = kv[P[j]];
     const uint64_t k = (uint64_t)__double_as_longlong(r.x);
-    for (int l = 1; l < ko.N; ++l) {
-      const uint64_t m = ko.bits[l] >= 64 ? ~0ull : ((1ull << ko.bits[l]) - 1ull);
-      ko.dst[l][j] = (uint32_t)((k >> ko.shift[l]) & m);
+    if (ko.mixed) {
+      uint32_t c[SPLATT_MAX_NMODES];
+      mixed_decode(ko.mr, k, c);
+      for (int l = 1; l < ko.N; ++l) ko.dst[l][j] = c[ko.qlev[l]];
+    } else {
+      for (int l = 1; l < ko.N; ++l) {
+        const uint64_t m = ko.bits[l] >= 64 ? ~0ull : ((1ull << ko.bits[l]) - 1ull);
+        ko.dst[l][j] = (uint32_t)((k >> ko.shift[l]) & m);
+      }
     }
     vout[j] = r.y;
   }
@@ -387,15 +608,31 @@ void sort_full(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
     }
     groups.push_back({0, hi});
   }
+  // One key group: a mixed-radix key when its fewer bits save a radix pass.
+  bool mixed = false;
+  int mixed_bits = 0;
+  uint64_t stride[SPLATT_MAX_NMODES] = {0};
+  if (groups.size() == 1) {
+    int total = 0;
+    for (int l = 0; l < N; ++l) total += bits[l];
+    unsigned __int128 prod = 1;
+    for (int l = N - 1; l >= 0; --l) {
+      stride[l] = (uint64_t)prod;
+      prod *= (unsigned __int128)std::max<uint64_t>(1, dims[perm[l]]);
+    }
+    while (mixed_bits < 64 && ((unsigned __int128)1 << mixed_bits) < prod) ++mixed_bits;
+    mixed = (mixed_bits + 7) / 8 < (total + 7) / 8 && !getenv("SPLATT_BUILD_PACKED");
+  }
   const int grid = grid_for(ctx, nnz);
   ArenaScope tmp_scope(current_arena(), true);  // sort buffers: released on return
+  // SPLATT_BUILD_CARRY (A/B runs): with one key group and the values on the device, the
+  // values' bits travel with the keys (8-byte payload) and the decode reads them in order
+  // instead of gathering them through the permutation.  Measured a tie on c5 (sort +3.0 ms,
+  // decode -2.7 ms; profiles/ab_r02/README.md), so the default keeps 4-byte positions.
+  const bool carry = groups.size() == 1 && !ctx->vals_pending && getenv("SPLATT_BUILD_CARRY");
   DevBuf<uint64_t> kA(nnz, st), kB(nnz, st);
-  DevBuf<uint32_t> pA(nnz, st), pB(nnz, st);
-  DevBuf<uint8_t> temp;
-  size_t temp_bytes = 0;
-  SB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, kA.p, kB.p, pA.p, pB.p, (int)nnz, 0,
-                                          64, st));
-  temp.alloc(temp_bytes, st);
+  DevBuf<uint32_t> pA(carry ? 0 : nnz, st), pB(carry ? 0 : nnz, st);
+  DevBuf<uint64_t> vA(carry ? nnz : 0, st), vB(carry ? nnz : 0, st);
   tr.mark("alloc");
   uint32_t* order = nullptr;  // current permutation (sorted position -> input position)
   for (size_t g = 0; g < groups.size(); ++g) {
@@ -404,18 +641,22 @@ void sort_full(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
     ks.hi = groups[g].second;
     int sh = 0;
     for (int l = ks.hi - 1; l >= ks.lo; --l) { ks.src[l] = lvl_src[l]; ks.shift[l] = sh; sh += bits[l]; }
-    const int total = sh;
+    ks.mixed = mixed;
+    for (int l = 0; l < N; ++l) ks.stride[l] = stride[l];
+    const int total = mixed ? mixed_bits : sh;
+    if (carry) {
+      pack_keys_kernel<<<grid, 256, 0, st>>>(ks, nnz, nullptr, kA.p, nullptr, d_vals, vA.p);
+      SB_CHECK_LAUNCH(ctx);
+      radix_sort_pairs(ctx, kA.p, vA.p, kB.p, vB.p, kA.p, vA.p, nnz, 0, total);
+      break;
+    }
     // order == nullptr: first group, positions are the identity (written into pA).
-    pack_keys_kernel<<<grid, 256, 0, st>>>(ks, nnz, order, kA.p, pA.p);
+    pack_keys_kernel<<<grid, 256, 0, st>>>(ks, nnz, order, kA.p, pA.p, nullptr, nullptr);
     SB_CHECK_LAUNCH(ctx);
     uint32_t* pin = order ? order : pA.p;
     uint32_t* pout = (pin == pB.p) ? pA.p : pB.p;
-    if (total > 0) {
-      SB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, kA.p, kB.p, pin, pout, (int)nnz, 0,
-                                              total, st));
-    } else {
-      SB_CUDA(cudaMemcpyAsync(pout, pin, nnz * 4, cudaMemcpyDeviceToDevice, st));
-    }
+    // (kA, pin) are scratch once read: they serve as the sort's alternate buffers
+    radix_sort_pairs(ctx, kA.p, pin, kB.p, pout, kA.p, pin, nnz, 0, total);
     order = pout;
   }
   tr.mark("pack+sort");
@@ -436,12 +677,23 @@ void sort_full(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* d_va
     for (int l = 0; l < N; ++l) ks.src[l] = nullptr;
     ks.lo = 0;
     ks.hi = N;
-    if (t.kv.p)
+    ks.mixed = mixed;
+    MixedRadix mr{};
+    mr.N = N;
+    for (int l = 0; l < N; ++l) {
+      mr.dim[l] = (uint32_t)std::max<uint64_t>(1, dims[perm[l]]);
+      mr.inv[l] = 1.0 / (double)mr.dim[l];
+    }
+    if (t.kv.p) {
       for (int l = 0; l < N; ++l) { t.shift[l] = ks.shift[l]; t.bits[l] = bits[l]; }
+      t.mixed = mixed;
+      t.mr = mr;
+    }
     decode_kernel<<<grid, 256, 0, st>>>(ks, BitSet{{bits[0], bits[1], bits[2], bits[3], bits[4],
                                                     bits[5], bits[6], bits[7]}},
-                                        co, nnz, kB.p, order, d_vals, t.vals.p,
-                                        t.kv.p);
+                                        mr, co, nnz, kB.p, carry ? nullptr : order,
+                                        carry ? reinterpret_cast<const double*>(vB.p) : d_vals,
+                                        t.vals.p, t.kv.p);
   } else {
     gather_kernel<<<grid, 256, 0, st>>>(co, nnz, order, d_vals, t.vals.p);
   }
@@ -543,10 +795,87 @@ void complete_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf
   out.tab.release();
 }
 
-// Levels of a tree from its sorted coordinates (number_levels + complete_levels).
+// Levels of a tree from its sorted coordinates by the two-pass count / write kernels (no
+// node-number arrays): counts per range, one host sync for the level sizes, then ids / ptr
+// (and a ROOT plan's records) written directly.  Moves t.coord[N-1] and t.vals into the tree.
+void write_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& out,
+                  Arena* out_arena, PhaseTrace& tr) {
+  cudaStream_t st = ctx->stream;
+  const int L = N - 1;
+  LevelIn li{};
+  li.N = N;
+  for (int l = 0; l < N; ++l) li.c[l] = t.coord[l].p;
+  RootPlanRecOut ro;
+  bool plan = false;
+  if (ctx->build_plan_ld > 0) {
+    ArenaScope o(out_arena, false);  // the plan lives as long as the tree
+    plan = root_plan_begin(ctx, out, li.c, t.vals.p, ctx->build_plan_ld, &ro);
+  }
+  // one range per CTA of a full persistent grid (8 CTAs of 256 threads per SM)
+  const uint64_t C = (uint64_t)ctx->num_sms * 8;
+  const uint64_t range = ceil_div(ceil_div(nnz, C), kLvTile) * kLvTile;
+  const int nranges = (int)ceil_div(nnz, range);
+  DevBuf<uint32_t> counts((size_t)nranges * L, st), totals(L, st);
+  auto count = [&](auto kern) { kern<<<nranges, 256, 0, st>>>(li, nnz, range, counts.p); };
+  switch (N) {
+    case 3: count(level_count_kernel<3>); break;
+    case 4: count(level_count_kernel<4>); break;
+    case 5: count(level_count_kernel<5>); break;
+    case 6: count(level_count_kernel<6>); break;
+    case 7: count(level_count_kernel<7>); break;
+    default: count(level_count_kernel<8>); break;
+  }
+  SB_CHECK_LAUNCH(ctx);
+  level_scan_kernel<<<1, 32, 0, st>>>(counts.p, nranges, L, totals.p);
+  SB_CHECK_LAUNCH(ctx);
+  std::vector<uint32_t> h(L, 0);
+  SB_CUDA(cudaMemcpyAsync(h.data(), totals.p, L * 4, cudaMemcpyDeviceToHost, st));
+  host_sync(ctx);
+  tr.mark("level counts");
+  LevelOut lo{};
+  for (int l = 0; l < L; ++l) {
+    out.nodes[l] = h[l];
+    ArenaScope o(out_arena, false);
+    out.ids[l].alloc(out.nodes[l], st);
+    out.ptr[l].alloc(out.nodes[l] + 1, st);
+    lo.ids[l] = out.ids[l].p;
+    lo.ptr[l] = out.ptr[l].p;
+  }
+  out.nodes[N - 1] = nnz;
+  auto write = [&](auto kern) {
+    kern<<<nranges, kLvThreads, 0, st>>>(li, nnz, range, counts.p, totals.p, lo, ro);
+  };
+  switch (N) {
+    case 3: write(level_write_kernel<3>); break;
+    case 4: write(level_write_kernel<4>); break;
+    case 5: write(level_write_kernel<5>); break;
+    case 6: write(level_write_kernel<6>); break;
+    case 7: write(level_write_kernel<7>); break;
+    default: write(level_write_kernel<8>); break;
+  }
+  SB_CHECK_LAUNCH(ctx);
+  tr.mark("level write");
+  if (plan) {
+    ArenaScope o(out_arena, false);
+    root_plan_end(ctx, out);
+    tr.mark("root plan");
+  }
+  out.ids[N - 1] = std::move(t.coord[N - 1]);
+  out.vals = std::move(t.vals);
+  out.tab_chunk = 0;
+  out.nchunks = 0;
+  out.tab.release();
+}
+
+// Levels of a tree from its sorted coordinates (write_levels; number_levels +
+// complete_levels when SPLATT_BUILD_SCATTER is set, for A/B runs).
 void finish_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& out,
                    Arena* out_arena, PhaseTrace& tr) {
   ArenaScope tmp_scope(current_arena(), true);
+  if (nnz > 0 && !getenv("SPLATT_BUILD_SCATTER")) {
+    write_levels(ctx, t, nnz, N, out, out_arena, tr);
+    return;
+  }
   LevelNumbering nb;
   number_levels(ctx, t, nnz, N, out, out_arena, nb, tr);
   complete_levels(ctx, t, nnz, N, out, out_arena, nb, tr);
@@ -636,14 +965,10 @@ void build_csf_set(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* 
         node_keys_kernel<<<grid, 256, 0, st>>>(qn.node[j].p, tq.coord[j].p, nnz, key.p, start.p,
                                                idx.p);
         SB_CHECK_LAUNCH(ctx);
-        size_t tb = 0;
-        SB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, skey.p, idx.p, sidx.p, (int)F,
-                                                0, nb, st));
         size_t tb2 = 0;
         SB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, sz.p, off.p, (int)F, st));
-        DevBuf<uint8_t> temp(std::max(tb, tb2), st);
-        SB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb, key.p, skey.p, idx.p, sidx.p, (int)F,
-                                                0, nb, st));
+        DevBuf<uint8_t> temp(tb2, st);
+        radix_sort_pairs(ctx, key.p, idx.p, skey.p, sidx.p, key.p, idx.p, F, 0, nb);
         const int gF = grid_for(ctx, F);
         node_sizes_kernel<<<gF, 256, 0, st>>>(sidx.p, start.p, F, nnz, sz.p);
         SB_CHECK_LAUNCH(ctx);
@@ -654,25 +979,22 @@ void build_csf_set(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* 
                                                nnz, perm_out.p, tr_.coord[0].p);
         SB_CHECK_LAUNCH(ctx);
       } else {
-        DevBuf<uint32_t> pos(nnz, st);
+        DevBuf<uint32_t> pos(nnz, st), tk(nnz, st);
         iota_kernel<<<grid, 256, 0, st>>>(pos.p, nnz);
         SB_CHECK_LAUNCH(ctx);
-        size_t temp_bytes = 0;
-        SB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, tq.coord[j].p,
-                                                tr_.coord[0].p, pos.p, perm_out.p, (int)nnz, 0,
-                                                nb, st));
-        DevBuf<uint8_t> temp(temp_bytes, st);
-        SB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, tq.coord[j].p,
-                                                tr_.coord[0].p, pos.p, perm_out.p, (int)nnz, 0,
-                                                nb, st));
+        radix_sort_pairs(ctx, tq.coord[j].p, pos.p, tr_.coord[0].p, perm_out.p, tk.p, pos.p, nnz,
+                         0, nb);
       }
       if (tq.kv.p) {
         KvOut ko{};
         ko.N = N;
+        ko.mixed = tq.mixed;
+        ko.mr = tq.mr;
         for (int l = 1; l < N; ++l) {
           ko.dst[l] = tr_.coord[l].p;
           ko.shift[l] = tq.shift[qlev[out.perm[l]]];
           ko.bits[l] = tq.bits[qlev[out.perm[l]]];
+          ko.qlev[l] = qlev[out.perm[l]];
         }
         gather_kv_kernel<<<grid, 256, 0, st>>>(ko, nnz, perm_out.p, tq.kv.p, tr_.vals.p);
       } else {
@@ -778,14 +1100,9 @@ void tile_tree(splatt_ctx* ctx, DevCsf& c, int T) {
   SB_CUDA(cudaMemsetAsync(cnt.p, 0, T * 8, st));
   tile_key_kernel<<<grid, 256, 0, st>>>(c.ids[N - 1].p, nnz, rows, T, key.p, pos.p, cnt.p);
   SB_CHECK_LAUNCH(ctx);
-  size_t sb = 0;
   int bits = 1;
   while ((1 << bits) < T) ++bits;
-  SB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sb, key.p, key2.p, pos.p, perm.p, (int)nnz, 0,
-                                          bits, st));
-  DevBuf<uint8_t> stemp(sb, st);
-  SB_CUDA(cub::DeviceRadixSort::SortPairs(stemp.p, sb, key.p, key2.p, pos.p, perm.p, (int)nnz, 0,
-                                          bits, st));
+  radix_sort_pairs(ctx, key.p, pos.p, key2.p, perm.p, key.p, pos.p, nnz, 0, bits);
   std::vector<unsigned long long> hcnt(T);
   SB_CUDA(cudaMemcpyAsync(hcnt.data(), cnt.p, T * 8, cudaMemcpyDeviceToHost, st));
   host_sync(ctx);

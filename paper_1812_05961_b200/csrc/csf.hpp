@@ -120,6 +120,20 @@ bool root_plan_begin(splatt_ctx* ctx, DevCsf& out, const uint32_t* const* coord,
                      const double* vals, int ld, RootPlanRecOut* ro);
 void root_plan_end(splatt_ctx* ctx, DevCsf& out);
 
+// Stable LSD radix sort (radix_sort.cu) of the pairs (src_k[i], src_v[i]) by key bits
+// [begin, end) into (out_k, out_v); (tmp_k, tmp_v) is scratch of n pairs and may be the
+// source itself (the source is read by the first pass only).  out and src must not alias.
+// Every buffer 16-byte aligned; n < 2^31.
+void radix_sort_pairs(splatt_ctx* ctx, const uint64_t* src_k, const uint32_t* src_v,
+                      uint64_t* out_k, uint32_t* out_v, uint64_t* tmp_k, uint32_t* tmp_v,
+                      uint64_t n, int begin, int end);
+void radix_sort_pairs(splatt_ctx* ctx, const uint64_t* src_k, const uint64_t* src_v,
+                      uint64_t* out_k, uint64_t* out_v, uint64_t* tmp_k, uint64_t* tmp_v,
+                      uint64_t n, int begin, int end);
+void radix_sort_pairs(splatt_ctx* ctx, const uint32_t* src_k, const uint32_t* src_v,
+                      uint32_t* out_k, uint32_t* out_v, uint32_t* tmp_k, uint32_t* tmp_v,
+                      uint64_t n, int begin, int end);
+
 // Ensure the chunk table for `chunk` leaves per work unit exists.
 void ensure_chunk_table(splatt_ctx* ctx, DevCsf& c, int chunk);
 

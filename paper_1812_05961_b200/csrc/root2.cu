@@ -11,8 +11,6 @@
 //      node's last child down to its last leaf.
 // Integer work only: the plan is a pure function of the tree (the hot set only decides
 // where a row is read from, never what is computed).
-#include <cub/cub.cuh>
-
 #include <algorithm>
 
 #include "mttkrp.hpp"
@@ -70,14 +68,23 @@ struct LevelOffsets {
   int N;
 };
 
-// Slot s <- the s-th most frequent (level, id) if it was sampled at least twice.
+// c -> ~c: an ascending stable sort of the complements is the descending stable sort of the
+// counts (equal counts keep the (level, id) order).
+__global__ void complement_kernel(uint32_t* __restrict__ c, uint64_t n) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
+       j += (uint64_t)gridDim.x * blockDim.x)
+    c[j] = ~c[j];
+}
+
+// Slot s <- the s-th most frequent (level, id) if it was sampled at least twice
+// (cnt_sorted: complemented counts in ascending order).
 __global__ void hot_slots_kernel(const uint32_t* __restrict__ cnt_sorted,
                                  const uint32_t* __restrict__ gidx_sorted, uint64_t total,
                                  uint32_t K, LevelOffsets lo, uint32_t* __restrict__ hot,
                                  uint32_t* __restrict__ slotmap) {
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= K) return;
-  if (s >= total || cnt_sorted[s] < 2) { hot[s] = ~0u; return; }
+  if (s >= total || ~cnt_sorted[s] < 2u) { hot[s] = ~0u; return; }
   const uint32_t g = gidx_sorted[s];
   int l = 1;
   while (l + 1 < lo.N && g >= lo.off[l + 1]) ++l;
@@ -143,20 +150,30 @@ struct CoordSet {
 // Every kSample-th leaf: its id, and the id of every internal node (levels 1..N-2) that
 // starts there — a level-l node starts at j when a coordinate of levels 0..l differs from
 // leaf j-1 (each node has one start, so nodes are sampled at the same 1/kSample rate).
+__device__ __forceinline__ void add_aggregated(uint32_t* cnt, uint32_t a) {
+  // equal addresses of a warp add once (power-law ids: the hot rows' counters are contended)
+  const uint32_t peers = __match_any_sync(0xffffffffu, a);
+  if (a != ~0u && (peers & ((1u << (threadIdx.x & 31u)) - 1u)) == 0u)
+    atomicAdd(&cnt[a], (uint32_t)__popc(peers));
+}
 __global__ void sampled_hist_coords_kernel(CoordSet cs, uint64_t nnz, LevelOffsets lo,
                                            uint32_t* __restrict__ cnt) {
   const int N = cs.N;
-  for (uint64_t k = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * kSample; k < nnz;
-       k += (uint64_t)gridDim.x * blockDim.x * kSample) {
-    atomicAdd(&cnt[lo.off[N - 1] + cs.c[N - 1][k]], 1u);
+  const uint64_t lane = threadIdx.x & 31u;
+  // warp-uniform loop (every lane takes part in the aggregation)
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u);
+       base * kSample < nnz; base += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = (base + lane) * kSample;
+    const bool valid = k < nnz;
+    add_aggregated(cnt, valid ? (uint32_t)(lo.off[N - 1] + cs.c[N - 1][k]) : ~0u);
     int ds = 0;  // first level whose coordinate differs from leaf k-1
-    if (k > 0) {
+    if (valid && k > 0) {
       ds = N - 1;
       for (int l = N - 2; l >= 0; --l)
         if (cs.c[l][k] != cs.c[l][k - 1]) ds = l;
     }
     for (int l = 1; l <= N - 2; ++l)
-      if (ds <= l) atomicAdd(&cnt[lo.off[l] + cs.c[l][k]], 1u);
+      add_aggregated(cnt, (valid && ds <= l) ? (uint32_t)(lo.off[l] + cs.c[l][k]) : ~0u);
   }
 }
 
@@ -245,12 +262,9 @@ void ensure_root_plan(splatt_ctx* ctx, DevCsf& c, int ld) {
     }
     iota_u32_kernel<<<grid_n(ctx, total), 256, 0, st>>>(gidx.p, total);
     SB_CHECK_LAUNCH(ctx);
-    size_t tb = 0;
-    SB_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cnt.p, cnt2.p, gidx.p, gidx2.p,
-                                                      (int)total, 0, 32, st));
-    DevBuf<uint8_t> temp(tb, st);
-    SB_CUDA(cub::DeviceRadixSort::SortPairsDescending(temp.p, tb, cnt.p, cnt2.p, gidx.p, gidx2.p,
-                                                      (int)total, 0, 32, st));
+    complement_kernel<<<grid_n(ctx, total), 256, 0, st>>>(cnt.p, total);
+    SB_CHECK_LAUNCH(ctx);
+    radix_sort_pairs(ctx, cnt.p, gidx.p, cnt2.p, gidx2.p, cnt.p, gidx.p, total, 0, 32);
     if (plan->K > 0) {
       hot_slots_kernel<<<(unsigned)ceil_div(plan->K, 256), 256, 0, st>>>(
           cnt2.p, gidx2.p, total, plan->K, lo, plan->hot.p, slotmap.p);
@@ -313,12 +327,9 @@ bool root_plan_begin(splatt_ctx* ctx, DevCsf& c, const uint32_t* const* coord,
     SB_CHECK_LAUNCH(ctx);
     iota_u32_kernel<<<grid_n(ctx, total), 256, 0, st>>>(gidx.p, total);
     SB_CHECK_LAUNCH(ctx);
-    size_t tb = 0;
-    SB_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cnt.p, cnt2.p, gidx.p, gidx2.p,
-                                                      (int)total, 0, 32, st));
-    DevBuf<uint8_t> temp(tb, st);
-    SB_CUDA(cub::DeviceRadixSort::SortPairsDescending(temp.p, tb, cnt.p, cnt2.p, gidx.p, gidx2.p,
-                                                      (int)total, 0, 32, st));
+    complement_kernel<<<grid_n(ctx, total), 256, 0, st>>>(cnt.p, total);
+    SB_CHECK_LAUNCH(ctx);
+    radix_sort_pairs(ctx, cnt.p, gidx.p, cnt2.p, gidx2.p, cnt.p, gidx.p, total, 0, 32);
     if (plan->K > 0) {
       hot_slots_kernel<<<(unsigned)ceil_div(plan->K, 256), 256, 0, st>>>(
           cnt2.p, gidx2.p, total, plan->K, lo, plan->hot.p, plan->slotmap.p);

@@ -94,6 +94,28 @@ def test_csf_host_input_and_wide_keys(sb, ctx):
     check_csf_equal(csf, t)
 
 
+def test_csf_bit_exact_mixed_radix_keys_and_sort_edges(sb, ctx):
+    # Dims whose mixed-radix composite key needs fewer radix passes than the bit-packed one
+    # (5x5x5: 9 -> 7 bits; 5^6: 18 -> 14 bits; the c5 dims: 57 -> 56 bits), so the builder
+    # sorts and decodes mixed-radix keys; nonzero counts around the radix sort's tile (4096
+    # pairs) and ragged ends (n % 4 != 0, n < 4: no bulk copy at all), and a c5-shaped tensor
+    # of 1.5M nonzeros (several tiles per sort range).
+    cases = [((5, 5, 5), n) for n in (1, 2, 3, 5, 100)]
+    cases += [((5, 5, 5, 5, 5, 5), 3000), ((200_000, 50_000, 10_000, 500), 4096),
+              ((200_000, 50_000, 10_000, 500), 4097), ((7, 300, 11), 8191)]
+    for i, (dims, nnz) in enumerate(cases):
+        rng = np.random.default_rng(100 + i)
+        ind = [rng.integers(0, d, nnz).astype(np.uint32) for d in dims]
+        vals = rng.random(nnz)
+        t = synth.SparseTensor(dims, ind, vals)
+        d_ind, d_vals = dev_coo(t)
+        check_csf_equal(sb.csf_build(d_ind, d_vals, dims, ctx=ctx), t)
+    t = synth.generate((200_000, 50_000, 10_000, 500), 1_500_000, [("zipf", 1.05)] * 4, "u01",
+                       seed=56)
+    d_ind, d_vals = dev_coo(t)
+    check_csf_equal(sb.csf_build(d_ind, d_vals, t.dims, ctx=ctx), t)
+
+
 # ---------------------------------------------------------------- MTTKRP
 def run_mttkrp(sb, ctx, t, F, mode, ld=None, pad_value=0.0):
     ind, vals = dev_coo(t)
