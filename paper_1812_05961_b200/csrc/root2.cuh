@@ -287,19 +287,21 @@ __global__ void __launch_bounds__(Threads<N>::k, 1) mttkrp_root2_kernel(const Ar
   // first half of a lane's 32-byte chunk sits at +16 in odd slots, see the prologue), cold
   // ones from global memory; predicated, so the warp runs one path whatever its groups mix.
   const uint32_t hot_sa = (uint32_t)__cvta_generic_to_shared(hotrows) + 8u * colc;
+  // this lane's column chunk of every gathered level's factor (loop-invariant bases)
+  const char* facb[N];
+#pragma unroll
+  for (int l = 1; l < N; ++l) facb[l] = reinterpret_cast<const char*>(a.fac[l] + colc);
   auto gather_en = [&](int l, uint32_t code, bool en) -> d4 {
     const uint32_t x = code & kIdMask;
     const uint32_t sa0 = hot_sa + x;
     return gather_pred(en, (code & kHot) != 0u, sa0, sa0 ^ 16u,
-                       reinterpret_cast<const double*>(
-                           reinterpret_cast<const char*>(a.fac[l] + colc) + x));
+                       reinterpret_cast<const double*>(facb[l] + x));
   };
   auto gather = [&](int l, uint32_t code) -> d4 {
     const uint32_t x = code & kIdMask;
     const uint32_t sa0 = hot_sa + x;
     return gather_on((code & kHot) != 0u, sa0, sa0 ^ 16u,
-                     reinterpret_cast<const double*>(
-                         reinterpret_cast<const char*>(a.fac[l] + colc) + x));
+                     reinterpret_cast<const double*>(facb[l] + x));
   };
   auto next_chunk = [&](uint32_t prev, bool first) -> uint32_t {
     if (a.work == nullptr) return first ? group : prev + ngroups;
