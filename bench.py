@@ -519,7 +519,9 @@ def main():
         "host_call_ms": 1e3 * statistics.mean(host_call_s[-args.steps:]),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": (f"mttkrp_csf_kernel<N={N}> ROOT traversal" if args.policy == "all"
+                     "kernel": ((f"mttkrp_root2_kernel<N={N}> ROOT traversal (second generation)"
+                                 if N == 4 else f"mttkrp_csf_kernel<N={N}> ROOT traversal")
+                                if args.policy == "all"
                                 else f"mttkrp_csf_kernel<N={N}> ROOT/INTERNAL/LEAF ({args.policy})"), "peak_source": peak_src,
                      "alg_bytes_per_launch": alg_bytes / max(1, launches),
                      # SURVEY.md §7 hard part 3: the compulsory-traffic view beside the

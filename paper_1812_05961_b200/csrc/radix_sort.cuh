@@ -80,8 +80,19 @@ __global__ void __launch_bounds__(1024) scan_kernel(uint32_t* __restrict__ count
   const int d = threadIdx.x % B, s = threadIdx.x / B;
   const int per = (nranges + S - 1) / S;
   const int c0 = min(nranges, s * per), c1 = min(nranges, c0 + per);
+  // (eight independent loads in flight per thread: the scan runs between two passes, so its
+  // latency is on the sort's critical path)
+  constexpr int U = 8;
   uint32_t sum = 0u;
-  for (int c = c0; c < c1; ++c) sum += counts[(size_t)c * B + d];
+  int c = c0;
+  for (; c + U <= c1; c += U) {
+    uint32_t v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = counts[(size_t)(c + u) * B + d];
+#pragma unroll
+    for (int u = 0; u < U; ++u) sum += v[u];
+  }
+  for (; c < c1; ++c) sum += counts[(size_t)c * B + d];
   part[s][d] = sum;
   __syncthreads();
   uint32_t total = 0u, before_slice = 0u;
@@ -113,7 +124,18 @@ __global__ void __launch_bounds__(1024) scan_kernel(uint32_t* __restrict__ count
   if (s == 0) dstart[d] = incl - total + ws[warp];
   __syncthreads();
   uint32_t run = dstart[d] + before_slice;
-  for (int c = c0; c < c1; ++c) {
+  c = c0;
+  for (; c + U <= c1; c += U) {
+    uint32_t v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = counts[(size_t)(c + u) * B + d];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      counts[(size_t)(c + u) * B + d] = run;
+      run += v[u];
+    }
+  }
+  for (; c < c1; ++c) {
     const uint32_t v = counts[(size_t)c * B + d];
     counts[(size_t)c * B + d] = run;
     run += v;
