@@ -135,7 +135,9 @@ struct FlagOut {
 };
 
 __device__ __forceinline__ uint32_t plan_code(const RootPlanRecOut& ro, uint64_t off, uint32_t id) {
-  const uint32_t s = ro.slotmap[off + id];  // (root2.cuh's row code: byte offset, bit 28 = hot)
+  // (read-only during the build's level kernels: the non-coherent path lets these loads
+  // move ahead of the record stores)
+  const uint32_t s = __ldg(ro.slotmap + off + id);  // (root2.cuh's row code: byte offset, bit 28 = hot)
   return s != ~0u ? ((1u << 28) | (s * ro.ldb + ((s & 1u) << 4))) : id * ro.ldb;
 }
 
@@ -323,7 +325,7 @@ __global__ void __launch_bounds__(kLvThreads) level_write_kernel(LevelIn li, uin
           const uint32_t code = plan_code(ro, ro.off_leaf, __ldg(li.c[N - 1] + j));
           const uint32_t fcode =
               dc <= (uint32_t)(N - 2) ? plan_code(ro, ro.off_fiber, __ldg(li.c[N - 2] + j)) : 0u;
-          const double v = ro.vals[j];
+          const double v = __ldg(ro.vals + j);
           ro.rec[j] = make_uint4(code | (dc << 29), fcode, (uint32_t)__double2loint(v),
                                  (uint32_t)__double2hiint(v));
         }

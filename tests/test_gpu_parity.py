@@ -116,6 +116,28 @@ def test_csf_bit_exact_mixed_radix_keys_and_sort_edges(sb, ctx):
     check_csf_equal(sb.csf_build(d_ind, d_vals, t.dims, ctx=ctx), t)
 
 
+def test_csf_bit_exact_adversarial_sort_inputs(sb, ctx):
+    # The radix sort's corner cases through the builder: every nonzero at one coordinate (one
+    # digit bucket takes all pairs in every pass, so the order is the input order alone), the
+    # input already in CSF order and in reverse order, and a single hot slice holding half
+    # the nonzeros across many sort tiles and ranges.
+    rng = np.random.default_rng(7)
+    n = 50_000
+    dims = (300, 200, 100)
+    cases = [[np.full(n, 7, np.uint32), np.full(n, 3, np.uint32), np.full(n, 99, np.uint32)]]
+    ind = [rng.integers(0, d, n).astype(np.uint32) for d in dims]
+    order = np.lexsort((ind[2], ind[1], ind[0]))
+    cases.append([a[order] for a in ind])
+    cases.append([a[order[::-1]] for a in ind])
+    hot = [rng.integers(0, d, n).astype(np.uint32) for d in dims]
+    hot[0][: n // 2] = 5
+    cases.append(hot)
+    for ind in cases:
+        t = synth.SparseTensor(dims, ind, rng.random(n))
+        d_ind, d_vals = dev_coo(t)
+        check_csf_equal(sb.csf_build(d_ind, d_vals, dims, ctx=ctx), t)
+
+
 # ---------------------------------------------------------------- MTTKRP
 def run_mttkrp(sb, ctx, t, F, mode, ld=None, pad_value=0.0):
     ind, vals = dev_coo(t)
