@@ -174,14 +174,14 @@ __global__ void level_flags_kernel(FlagOut f, uint64_t nnz, RootPlanRecOut ro) {
 }
 
 // ---- Levels of a tree in two passes over its sorted coordinates, without node-number arrays
-// (the derived trees).  The leaves are split into contiguous ranges, one per
-// CTA of a persistent grid.  Pass 1 counts the node starts of every internal level in each
-// range; a small scan turns the counts into each range's first node index per level (and the
-// level totals, which size ids/ptr); pass 2 recomputes the starts, numbers them by a block
-// scan on top of the range's running index, and writes ids/ptr (and a ROOT plan's per-leaf
-// records) directly.
-constexpr int kLvThreads = 256, kLvPer = 4;                 // rows of 32 leaves per warp step
-constexpr int kLvTile = kLvThreads * kLvPer;                // leaves per CTA step in pass 2
+// (the derived trees).  The leaves are split into contiguous ranges of whole
+// 32-leaf rows, one per warp of a full grid.  Pass 1 counts the node starts of every internal
+// level in each range (ballots); a scan turns the counts into each range's first node index
+// per level (and the level totals, which size ids/ptr); pass 2 walks each range row by row,
+// numbers the starts by ballot + popc on top of the range's running index — no block-level
+// synchronisation anywhere — and writes ids/ptr (and a ROOT plan's per-leaf records) directly.
+constexpr int kLvThreads = 256;
+constexpr int kLvWarps = kLvThreads / 32;
 
 struct LevelIn {
   const uint32_t* c[SPLATT_MAX_NMODES];  // sorted coordinates per level (nnz each)
@@ -200,44 +200,81 @@ __device__ __forceinline__ int first_diff(const LevelIn& li, uint64_t j) {
   return d;
 }
 
-// counts[r * (N-1) + l] = node starts of level l among the leaves of range r.
+// counts[l * nwr + w] = node starts of level l among the leaves of warp range w.
 template <int N>
-__global__ void __launch_bounds__(256) level_count_kernel(LevelIn li, uint64_t nnz, uint64_t range,
-                                                          uint32_t* __restrict__ counts) {
+__global__ void __launch_bounds__(kLvThreads) level_count_kernel(LevelIn li, uint64_t nnz,
+                                                                 uint64_t range, uint32_t nwr,
+                                                                 uint32_t* __restrict__ counts) {
   constexpr int L = N - 1;
-  __shared__ uint32_t sc[SPLATT_MAX_NMODES];
-  if (threadIdx.x < SPLATT_MAX_NMODES) sc[threadIdx.x] = 0u;
-  __syncthreads();
-  uint32_t cnt[SPLATT_MAX_NMODES] = {0};
-  const uint64_t lo = blockIdx.x * range, hi = min(nnz, lo + range);
-  for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
-    const int d = first_diff<N>(li, j);
+  const uint32_t w = blockIdx.x * kLvWarps + (threadIdx.x >> 5);
+  if (w >= nwr) return;
+  const int lane = threadIdx.x & 31;
+  const uint64_t r0 = w * range, r1 = min(nnz, r0 + range);
+  uint32_t cnt[L];
 #pragma unroll
-    for (int l = 0; l < L; ++l) cnt[l] += (d <= l) ? 1u : 0u;
+  for (int l = 0; l < L; ++l) cnt[l] = 0u;
+  for (uint64_t j0 = r0; j0 < r1; j0 += 32) {
+    const uint64_t j = j0 + lane;
+    const int d = (j < r1) ? first_diff<N>(li, j) : N - 1;
+#pragma unroll
+    for (int l = 0; l < L; ++l) cnt[l] += (uint32_t)__popc(__ballot_sync(0xffffffffu, d <= l));
   }
+  if (lane < L) {
 #pragma unroll
-  for (int l = 0; l < L; ++l) {
-    uint32_t v = cnt[l];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&sc[l], v);
+    for (int l = 0; l < L; ++l)
+      if (lane == l) counts[(size_t)l * nwr + w] = cnt[l];
   }
-  __syncthreads();
-  if (threadIdx.x < L) counts[(size_t)blockIdx.x * L + threadIdx.x] = sc[threadIdx.x];
 }
 
-// In place: counts[r][l] -> sum over ranges r' < r; totals[l] = the level's node count.
-__global__ void level_scan_kernel(uint32_t* __restrict__ counts, int nranges, int L,
-                                  uint32_t* __restrict__ totals) {
-  const int l = threadIdx.x;
-  if (l >= L) return;
-  uint32_t run = 0u;
-  for (int r = 0; r < nranges; ++r) {
-    const uint32_t v = counts[(size_t)r * L + l];
-    counts[(size_t)r * L + l] = run;
-    run += v;
+// In place, one CTA of 1024 threads per level: counts[l][w] -> sum over ranges w' < w;
+// totals[l] = the level's node count.
+__global__ void __launch_bounds__(1024) level_scan_kernel(uint32_t* __restrict__ counts,
+                                                          uint32_t nwr,
+                                                          uint32_t* __restrict__ totals) {
+  __shared__ uint32_t ws[32];
+  uint32_t* c = counts + (size_t)blockIdx.x * nwr;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t carry = 0u;
+  for (uint32_t b = 0; b < nwr; b += 1024) {
+    const uint32_t i = b + threadIdx.x;
+    const uint32_t v = i < nwr ? c[i] : 0u;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) ws[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t x = ws[lane];
+      uint32_t xi = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, xi, o);
+        if (lane >= o) xi += y;
+      }
+      ws[lane] = xi - x;
+    }
+    __syncthreads();
+    const uint32_t excl = carry + ws[warp] + incl - v;
+    if (i < nwr) c[i] = excl;
+    const uint32_t last = __shfl_sync(0xffffffffu, excl + v, 31);  // (warp 31's: the chunk's end)
+    __syncthreads();
+    if (warp == 31 && lane == 0) ws[0] = last;
+    __syncthreads();
+    carry = ws[0];
+    __syncthreads();
   }
-  totals[l] = run;
+  if (threadIdx.x == 0) totals[blockIdx.x] = carry;
+}
+
+// flag[k] = 1 iff a level-j node starts at leaf k (inclusive-scanned into node numbers).
+template <int N>
+__global__ void level_start_kernel(LevelIn li, uint64_t nnz, int j, uint32_t* __restrict__ flag) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (uint64_t)gridDim.x * blockDim.x)
+    flag[k] = (first_diff<N>(li, k) <= j) ? 1u : 0u;
 }
 
 struct LevelOut {
@@ -245,102 +282,62 @@ struct LevelOut {
   uint32_t* ptr[SPLATT_MAX_NMODES];
 };
 
-// Pass 2.  A step of the CTA covers kLvTile leaves, warp w the kLvPer rows of 32 consecutive
-// leaves at [step + 256 w, step + 256 (w + 1)): every load and store is a coalesced row.  A
-// leaf's node starts at level l are the ballot of (d <= l) over its row; its node index is the
-// range's running base + the starts of the lower warps (shared memory) + of the earlier rows
-// of its warp + of the lower lanes of its row (popc of the ballot).
+// Pass 2: warp w walks its range in rows of 32 consecutive leaves (coalesced loads and record
+// stores).  A leaf's node starts at level l are the ballot of (d <= l) over its row; its node
+// index is the range's first index + the starts of the earlier rows + of the lower lanes of its
+// row.
 template <int N>
 __global__ void __launch_bounds__(kLvThreads) level_write_kernel(LevelIn li, uint64_t nnz,
-                                                                 uint64_t range,
+                                                                 uint64_t range, uint32_t nwr,
                                                                  const uint32_t* __restrict__ bases,
                                                                  const uint32_t* __restrict__ totals,
                                                                  LevelOut lo, RootPlanRecOut ro) {
   constexpr int L = N - 1;
-  constexpr int kWarps = kLvThreads / 32;
-  __shared__ uint32_t s_cnt[kWarps][L];
-  __shared__ uint32_t s_base[L];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t w = blockIdx.x * kLvWarps + (threadIdx.x >> 5);
+  if (w >= nwr) return;
+  const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
-  const uint64_t r0 = blockIdx.x * range, r1 = min(nnz, r0 + range);
-  if (threadIdx.x < L) s_base[threadIdx.x] = bases[(size_t)blockIdx.x * L + threadIdx.x];
-  uint32_t pend[L];  // last warp: the range's running bases after its step
-  for (uint64_t step = r0; step < r1; step += kLvTile) {
-    const uint64_t wb = step + (uint64_t)warp * 32u * kLvPer;
-    int d[kLvPer];
-    uint32_t ball[kLvPer][L];
-    uint32_t wcnt[L];
+  const uint64_t r0 = w * range, r1 = min(nnz, r0 + range);
+  uint32_t next[L];  // index of the range's next start per level
 #pragma unroll
-    for (int l = 0; l < L; ++l) wcnt[l] = 0u;
-#pragma unroll
-    for (int i = 0; i < kLvPer; ++i) {
-      const uint64_t j = wb + (uint64_t)i * 32u + lane;
-      d[i] = (j < r1) ? first_diff<N>(li, j) : N - 1;
-#pragma unroll
-      for (int l = 0; l < L; ++l) {
-        ball[i][l] = __ballot_sync(0xffffffffu, d[i] <= l);
-        wcnt[l] += (uint32_t)__popc(ball[i][l]);
-      }
-    }
-    __syncthreads();  // s_cnt / s_base of the previous step consumed by every warp
-    if (lane < L) {
-#pragma unroll
-      for (int l = 0; l < L; ++l)
-        if (lane == l) {
-          s_cnt[warp][l] = wcnt[l];
-          if (warp == kWarps - 1 && step > r0) s_base[l] = pend[l];  // previous step's end
-        }
-    }
-    __syncthreads();
-    uint32_t next[L];  // index of this warp's next start per level (before its rows)
+  for (int l = 0; l < L; ++l) next[l] = __ldg(bases + (size_t)l * nwr + w);
+  for (uint64_t j0 = r0; j0 < r1; j0 += 32) {
+    const uint64_t j = j0 + lane;
+    const bool valid = j < r1;
+    const int d = valid ? first_diff<N>(li, j) : N - 1;
+    uint32_t k[L];
 #pragma unroll
     for (int l = 0; l < L; ++l) {
-      uint32_t off = s_base[l];
-      for (int x = 0; x < warp; ++x) off += s_cnt[x][l];
-      next[l] = off;
+      const uint32_t b = __ballot_sync(0xffffffffu, d <= l);
+      k[l] = next[l] + (uint32_t)__popc(b & lt);
+      next[l] += (uint32_t)__popc(b);
     }
+    int dn = 0;  // d of leaf j+1: the shallowest node ending at leaf j (0 at the last leaf)
+    if (ro.rec) dn = __shfl_down_sync(0xffffffffu, d, 1);
+    if (!valid) continue;
+    // nodes starting at leaf j: levels d .. L-1, each one's first child starts here too
 #pragma unroll
-    for (int i = 0; i < kLvPer; ++i) {
-      const uint64_t j = wb + (uint64_t)i * 32u + lane;
-      const bool valid = j < r1;
-      uint32_t k[L];
-#pragma unroll
-      for (int l = 0; l < L; ++l) {
-        k[l] = next[l] + (uint32_t)__popc(ball[i][l] & lt);
-        next[l] += (uint32_t)__popc(ball[i][l]);
-      }
-      if (valid) {
-#pragma unroll
-        for (int l = 0; l < L; ++l) {
-          if (l >= d[i]) {
-            lo.ids[l][k[l]] = __ldg(li.c[l] + j);
-            lo.ptr[l][k[l]] = (l == L - 1) ? (uint32_t)j : k[l + 1 < L ? l + 1 : l];
-          }
-        }
-        if (ro.rec) {
-          // d of leaf j+1: the shallowest node ending at leaf j (0 at the last leaf)
-          int dn = __shfl_down_sync(0xffffffffu, d[i], 1);
-          if (lane == 31 || j + 1 >= r1) dn = (j + 1 < nnz) ? first_diff<N>(li, j + 1) : 0;
-          const uint32_t dc = (uint32_t)dn;
-          const uint32_t code = plan_code(ro, ro.off_leaf, __ldg(li.c[N - 1] + j));
-          const uint32_t fcode =
-              dc <= (uint32_t)(N - 2) ? plan_code(ro, ro.off_fiber, __ldg(li.c[N - 2] + j)) : 0u;
-          const double v = __ldg(ro.vals + j);
-          ro.rec[j] = make_uint4(code | (dc << 29), fcode, (uint32_t)__double2loint(v),
-                                 (uint32_t)__double2hiint(v));
-        }
-        if (j + 1 == nnz) {
-#pragma unroll
-          for (int l = 0; l < L; ++l)
-            lo.ptr[l][totals[l]] = (l + 1 < L) ? totals[l + 1] : (uint32_t)nnz;
-        }
-      } else if (ro.rec) {
-        (void)__shfl_down_sync(0xffffffffu, d[i], 1);  // (every lane takes part)
+    for (int l = 0; l < L; ++l) {
+      if (l >= d) {
+        lo.ids[l][k[l]] = __ldg(li.c[l] + j);
+        lo.ptr[l][k[l]] = (l == L - 1) ? (uint32_t)j : k[l + 1 < L ? l + 1 : l];
       }
     }
-    // the last warp's final indices are the next step's bases (stored after the next barrier)
+    if (ro.rec) {
+      if (lane == 31 || j + 1 >= r1) dn = (j + 1 < nnz) ? first_diff<N>(li, j + 1) : 0;
+      const uint32_t dc = (uint32_t)dn;
+      const uint32_t code = plan_code(ro, ro.off_leaf, __ldg(li.c[N - 1] + j));
+      const uint32_t fcode =
+          dc <= (uint32_t)(N - 2) ? plan_code(ro, ro.off_fiber, __ldg(li.c[N - 2] + j)) : 0u;
+      const double v = __ldg(ro.vals + j);
+      ro.rec[j] = make_uint4(code | (dc << 29), fcode, (uint32_t)__double2loint(v),
+                             (uint32_t)__double2hiint(v));
+    }
+    if (j + 1 == nnz) {
 #pragma unroll
-    for (int l = 0; l < L; ++l) pend[l] = next[l];
+      for (int l = 0; l < L; ++l)
+        lo.ptr[l][totals[l]] = (l + 1 < L) ? totals[l + 1] : (uint32_t)nnz;
+    }
   }
 }
 
@@ -800,8 +797,53 @@ void complete_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf
 // Levels of a tree from its sorted coordinates by the two-pass count / write kernels (no
 // node-number arrays): counts per range, one host sync for the level sizes, then ids / ptr
 // (and a ROOT plan's records) written directly.  Moves t.coord[N-1] and t.vals into the tree.
+// Pass 1 of the level kernels (counts, scan, one host sync for the level sizes).
+struct LevelCounts {
+  DevBuf<uint32_t> counts, totals;  // per-range first indices (after the scan), level sizes
+  uint64_t range = 0;
+  uint32_t nwr = 0;
+  std::vector<uint32_t> h;          // level sizes on the host
+};
+
+void count_levels(splatt_ctx* ctx, const SortedTree& t, uint64_t nnz, int N, LevelCounts& lc) {
+  cudaStream_t st = ctx->stream;
+  const int L = N - 1;
+  LevelIn li{};
+  li.N = N;
+  for (int l = 0; l < N; ++l) li.c[l] = t.coord[l].p;
+  // one range of whole rows per warp of a full grid (8 CTAs of 8 warps per SM)
+  const uint64_t W = (uint64_t)ctx->num_sms * 8 * kLvWarps;
+  const uint64_t range = ceil_div(ceil_div(nnz, W), 32) * 32;
+  const uint32_t nwr = (uint32_t)ceil_div(nnz, range);
+  const unsigned blocks = (unsigned)ceil_div(nwr, kLvWarps);
+  lc.range = range;
+  lc.nwr = nwr;
+  lc.counts.alloc((size_t)nwr * L, st);
+  lc.totals.alloc(L, st);
+  DevBuf<uint32_t>& counts = lc.counts;
+  DevBuf<uint32_t>& totals = lc.totals;
+  auto count = [&](auto kern) {
+    kern<<<blocks, kLvThreads, 0, st>>>(li, nnz, range, nwr, counts.p);
+  };
+  switch (N) {
+    case 3: count(level_count_kernel<3>); break;
+    case 4: count(level_count_kernel<4>); break;
+    case 5: count(level_count_kernel<5>); break;
+    case 6: count(level_count_kernel<6>); break;
+    case 7: count(level_count_kernel<7>); break;
+    default: count(level_count_kernel<8>); break;
+  }
+  SB_CHECK_LAUNCH(ctx);
+  level_scan_kernel<<<L, 1024, 0, st>>>(counts.p, nwr, totals.p);
+  SB_CHECK_LAUNCH(ctx);
+  lc.h.assign(L, 0);
+  SB_CUDA(cudaMemcpyAsync(lc.h.data(), totals.p, L * 4, cudaMemcpyDeviceToHost, st));
+  host_sync(ctx);
+}
+
+// Levels of a tree by the two-pass count / write kernels (`pre`: pass 1 already run).
 void write_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& out,
-                  Arena* out_arena, PhaseTrace& tr) {
+                  Arena* out_arena, PhaseTrace& tr, LevelCounts* pre = nullptr) {
   cudaStream_t st = ctx->stream;
   const int L = N - 1;
   LevelIn li{};
@@ -813,27 +855,16 @@ void write_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& o
     ArenaScope o(out_arena, false);  // the plan lives as long as the tree
     plan = root_plan_begin(ctx, out, li.c, t.vals.p, ctx->build_plan_ld, &ro);
   }
-  // one range per CTA of a full persistent grid (8 CTAs of 256 threads per SM)
-  const uint64_t C = (uint64_t)ctx->num_sms * 8;
-  const uint64_t range = ceil_div(ceil_div(nnz, C), kLvTile) * kLvTile;
-  const int nranges = (int)ceil_div(nnz, range);
-  DevBuf<uint32_t> counts((size_t)nranges * L, st), totals(L, st);
-  auto count = [&](auto kern) { kern<<<nranges, 256, 0, st>>>(li, nnz, range, counts.p); };
-  switch (N) {
-    case 3: count(level_count_kernel<3>); break;
-    case 4: count(level_count_kernel<4>); break;
-    case 5: count(level_count_kernel<5>); break;
-    case 6: count(level_count_kernel<6>); break;
-    case 7: count(level_count_kernel<7>); break;
-    default: count(level_count_kernel<8>); break;
-  }
-  SB_CHECK_LAUNCH(ctx);
-  level_scan_kernel<<<1, 32, 0, st>>>(counts.p, nranges, L, totals.p);
-  SB_CHECK_LAUNCH(ctx);
-  std::vector<uint32_t> h(L, 0);
-  SB_CUDA(cudaMemcpyAsync(h.data(), totals.p, L * 4, cudaMemcpyDeviceToHost, st));
-  host_sync(ctx);
+  LevelCounts own;
+  LevelCounts& lc = pre ? *pre : own;
+  if (!pre) count_levels(ctx, t, nnz, N, lc);
   tr.mark("level counts");
+  const std::vector<uint32_t>& h = lc.h;
+  const uint64_t range = lc.range;
+  const uint32_t nwr = lc.nwr;
+  const unsigned blocks = (unsigned)ceil_div(nwr, kLvWarps);
+  DevBuf<uint32_t>& counts = lc.counts;
+  DevBuf<uint32_t>& totals = lc.totals;
   LevelOut lo{};
   for (int l = 0; l < L; ++l) {
     out.nodes[l] = h[l];
@@ -845,7 +876,7 @@ void write_levels(splatt_ctx* ctx, SortedTree& t, uint64_t nnz, int N, DevCsf& o
   }
   out.nodes[N - 1] = nnz;
   auto write = [&](auto kern) {
-    kern<<<nranges, kLvThreads, 0, st>>>(li, nnz, range, counts.p, totals.p, lo, ro);
+    kern<<<blocks, kLvThreads, 0, st>>>(li, nnz, range, nwr, counts.p, totals.p, lo, ro);
   };
   switch (N) {
     case 3: write(level_write_kernel<3>); break;
@@ -943,8 +974,40 @@ void build_csf_set(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* 
     if (k != qtree && qlev[roots[k]] >= 1 && qlev[roots[k]] <= N - 2) blocks = true;
   // (the numbering is needed anyway; only its node counts decide, per tree, below)
   if (getenv("SPLATT_BUILD_NOBLOCKS")) blocks = false;  // A/B runs: leaf re-sorts only
+  // Q's level sizes (pass 1 of its level kernels, reused at its write below) decide the
+  // block trees; their per-leaf node numbers at the root level are flag + scan.
+  LevelCounts qc;
   LevelNumbering qn;
-  if (blocks) number_levels(ctx, tq, nnz, N, *outs[qtree], out_arena, qn, tr);
+  if (blocks) {
+    count_levels(ctx, tq, nnz, N, qc);
+    for (int l = 0; l < N - 1; ++l) qn.counts[l] = qc.h[l];
+    qn.counts[N - 1] = nnz;
+    for (int k = 0; k < ntrees; ++k) {
+      const int j = qlev[roots[k]];
+      if (k == qtree || j < 1 || j > N - 2 || nnz < kBlockLeaves * qn.counts[j] || qn.node[j].p)
+        continue;
+      qn.node[j].alloc(nnz, st);
+      LevelIn li{};
+      li.N = N;
+      for (int l = 0; l < N; ++l) li.c[l] = tq.coord[l].p;
+      auto start = [&](auto kern) { kern<<<grid, 256, 0, st>>>(li, nnz, j, qn.node[j].p); };
+      switch (N) {
+        case 3: start(level_start_kernel<3>); break;
+        case 4: start(level_start_kernel<4>); break;
+        case 5: start(level_start_kernel<5>); break;
+        case 6: start(level_start_kernel<6>); break;
+        case 7: start(level_start_kernel<7>); break;
+        default: start(level_start_kernel<8>); break;
+      }
+      SB_CHECK_LAUNCH(ctx);
+      ArenaScope tmp_scope(current_arena(), true);
+      size_t tb = 0;
+      SB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, qn.node[j].p, qn.node[j].p, (int)nnz, st));
+      DevBuf<uint8_t> temp(tb, st);
+      SB_CUDA(cub::DeviceScan::InclusiveSum(temp.p, tb, qn.node[j].p, qn.node[j].p, (int)nnz, st));
+    }
+    tr.mark("Q levels");
+  }
   for (int k = 0; k < ntrees; ++k) {
     if (k == qtree) continue;
     DevCsf& out = *outs[k];
@@ -1014,7 +1077,7 @@ void build_csf_set(splatt_ctx* ctx, const uint32_t* const* d_ind, const double* 
     finish_levels(ctx, tr_, nnz, N, out, out_arena, tr);
   }
   if (qtree >= 0) {
-    if (blocks) complete_levels(ctx, tq, nnz, N, *outs[qtree], out_arena, qn, tr);
+    if (blocks) write_levels(ctx, tq, nnz, N, *outs[qtree], out_arena, tr, &qc);
     else finish_levels(ctx, tq, nnz, N, *outs[qtree], out_arena, tr);
   }
 }
