@@ -188,8 +188,8 @@ int main(int argc, char** argv) {
     uint32_t* rv;
     printf("  %-28s %8.3f ms\n", "cub SortPairs", cub_sort<U64>(ka, kc, va, vc, n, 57, s, &rk, &rv));
     trial<U64, 8, 256, 12>("sort 8b 256x12", k, v, ka, kb, va, vb, n, 57, rk, rv, s);
-    trial<U64, 8, 512, 8>("sort 8b 512x8", k, v, ka, kb, va, vb, n, 57, rk, rv, s);
-    trial<U64, 8, 512, 6>("sort 8b 512x6", k, v, ka, kb, va, vb, n, 57, rk, rv, s);
+    trial<U64, 8, 256, 8>("sort 8b 256x8", k, v, ka, kb, va, vb, n, 57, rk, rv, s);
+    trial<U64, 8, 256, 10>("sort 8b 256x10", k, v, ka, kb, va, vb, n, 57, rk, rv, s);
     trial<U64, 8, 256, 16>("sort 8b 256x16", k, v, ka, kb, va, vb, n, 57, rk, rv, s);
     {
       // (key, 64-bit value): timing only
@@ -233,8 +233,8 @@ int main(int argc, char** argv) {
     printf("  %-28s %8.3f ms\n", "cub SortPairs",
            cub_sort<uint32_t>(k32a, k32c, va, vc, n, bits, s, &rk, &rv));
     trial<uint32_t, 8, 512, 16>("sort 8b 512x16", k32, v, k32a, k32b, va, vb, n, bits, rk, rv, s);
-    trial<uint32_t, 8, 512, 8>("sort 8b 512x8", k32, v, k32a, k32b, va, vb, n, bits, rk, rv, s);
-    trial<uint32_t, 8, 512, 12>("sort 8b 512x12", k32, v, k32a, k32b, va, vb, n, bits, rk, rv, s);
+    trial<uint32_t, 8, 256, 8>("sort 8b 256x8", k32, v, k32a, k32b, va, vb, n, bits, rk, rv, s);
+    trial<uint32_t, 8, 256, 12>("sort 8b 256x12", k32, v, k32a, k32b, va, vb, n, bits, rk, rv, s);
     trial<uint32_t, 8, 256, 16>("sort 8b 256x16", k32, v, k32a, k32b, va, vb, n, bits, rk, rv, s);
     trial<uint32_t, 8, 256, 24>("sort 8b 256x24", k32, v, k32a, k32b, va, vb, n, bits, rk, rv, s);
   }
