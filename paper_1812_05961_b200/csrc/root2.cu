@@ -28,6 +28,19 @@
 
 namespace sb {
 
+#ifndef SB_ROOT2_HOT_MAX
+#define SB_ROOT2_HOT_MAX 2
+#endif
+// Hot rows held in shared memory (at most; SPLATT_ROOT2_HOT overrides).  Only the very top
+// rows pay: a power-law tensor sends ~1/H of a level's gathers to its hottest row, so every
+// SM hammers one L2 line; rows further down the list are read by different groups of a warp
+// in one instruction and cost shared-memory bank conflicts instead (c5 sweep: K = 0 2.66,
+// 2 2.39, 8 2.45, 32 2.50, 248 (the capacity) 2.56 ms; profiles/ab_r02/README.md).
+uint32_t root2_hot_rows() {
+  if (const char* e = getenv("SPLATT_ROOT2_HOT")) return (uint32_t)atoi(e);
+  return SB_ROOT2_HOT_MAX;
+}
+
 int root2_table_chunk() {
   if (const char* e = getenv("SPLATT_CHUNK")) {
     const int v = atoi(e);
@@ -231,7 +244,7 @@ void ensure_root_plan(splatt_ctx* ctx, DevCsf& c, int ld) {
   auto plan = std::make_unique<RootPlan>();
   plan->ld = ld;
   plan->K = root2_hot_capacity(N, ld);
-  if (const char* e = getenv("SPLATT_ROOT2_HOT")) plan->K = std::min<uint32_t>(plan->K, atoi(e));
+  plan->K = std::min<uint32_t>(plan->K, root2_hot_rows());
   const uint32_t ldb = (uint32_t)ld * 8u;
   LevelOffsets lo{};
   lo.N = N;
@@ -301,7 +314,7 @@ bool root_plan_begin(splatt_ctx* ctx, DevCsf& c, const uint32_t* const* coord,
   auto plan = std::make_unique<RootPlan>();  // from the current arena (the tree's)
   plan->ld = ld;
   plan->K = root2_hot_capacity(N, ld);
-  if (const char* e = getenv("SPLATT_ROOT2_HOT")) plan->K = std::min<uint32_t>(plan->K, atoi(e));
+  plan->K = std::min<uint32_t>(plan->K, root2_hot_rows());
   LevelOffsets lo{};
   lo.N = N;
   uint64_t total = 0;

@@ -55,7 +55,10 @@ struct Threads { static constexpr int k = (N == 3) ? SB_ROOT2_THREADS3 : SB_ROOT
 #define SB_ROOT2_B 48
 #endif
 constexpr int kBMax = SB_ROOT2_B;           // leaves per staged batch (at most)
-constexpr int kRecBudget = 200 * 1024;      // record buffers of all groups of a CTA (at most)
+#ifndef SB_ROOT2_RECBUDGET_KB
+#define SB_ROOT2_RECBUDGET_KB 200
+#endif
+constexpr int kRecBudget = SB_ROOT2_RECBUDGET_KB * 1024;  // record buffers of all groups (at most)
 constexpr int kSmemBudget = 225 * 1024;     // dynamic shared memory per CTA
 
 struct d4 { double x, y, z, w; };
