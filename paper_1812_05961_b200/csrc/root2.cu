@@ -32,10 +32,12 @@ namespace sb {
 #define SB_ROOT2_HOT_MAX 2
 #endif
 // Hot rows held in shared memory (at most; SPLATT_ROOT2_HOT overrides).  Only the very top
-// rows pay: a power-law tensor sends ~1/H of a level's gathers to its hottest row, so every
-// SM hammers one L2 line; rows further down the list are read by different groups of a warp
-// in one instruction and cost shared-memory bank conflicts instead (c5 sweep: K = 0 2.66,
-// 2 2.39, 8 2.45, 32 2.50, 248 (the capacity) 2.56 ms; profiles/ab_r02/README.md).
+// rows pay: a power-law tensor sends ~1/H of a level's gathers to its hottest row, and those
+// reads then skip the L1TEX/L2 round trip (per-CTA replicas of the same rows in global memory,
+// which would relieve an L2 hot spot, ran as K = 0); rows further down the list are read by
+// different groups of a warp in one instruction and cost shared-memory bank conflicts instead
+// (c5 sweep: K = 0 2.66, 2 2.39, 8 2.45, 32 2.50, 248 (the capacity) 2.56 ms;
+// profiles/ab_r02/README.md).
 uint32_t root2_hot_rows() {
   if (const char* e = getenv("SPLATT_ROOT2_HOT")) return (uint32_t)atoi(e);
   return SB_ROOT2_HOT_MAX;
