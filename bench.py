@@ -345,6 +345,9 @@ def main():
                          "auto = the library's: half-L2 tiles in runs of >= 10 iterations)")
     ap.add_argument("--partition", default="auto", choices=["auto", "nnz", "slices"],
                     help="multi-GPU split: per-mode auto, equal nonzero ranges (P2), whole slices (P1)")
+    ap.add_argument("--exchange", default="collective", choices=["collective", "peer"],
+                    help="multi-GPU factor-row exchange: NCCL all-gather after the solve (default), "
+                         "or the solve kernel storing its rows into the peers' matrices over NVLink")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -391,6 +394,7 @@ def main():
     if world > 1:
         ctx.set_comm()
         ctx.set_partition(args.partition)
+        ctx.set_exchange(args.exchange)
 
     N = len(t.dims)
     R, iters = cfg["rank"], cfg["iters"]
@@ -548,7 +552,9 @@ def main():
                          "ncu_source": ncu_rec.get("source"),
                      }},
         "comm": {"backend": "nccl" if world > 1 else None,
-                 "nranks": int(st[0].get("nranks", 1)) if st else None},
+                 "nranks": int(st[0].get("nranks", 1)) if st else None,
+                 "exchange": ("peer stores from the solve kernel" if st and st[0].get("exchange")
+                              else "nccl all-gather") if world > 1 else None},
         "gpu_launches": sum(s["kernel_launches"] for s in st),
         "clocks": clk.summary() if clk else None,
         "e2e": e2e,

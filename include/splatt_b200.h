@@ -122,6 +122,8 @@ typedef struct {
   double   t_aux_fit;       /*   and fit spans: overlapped with MTTKRP, not in t_inverse  */
   double   mttkrp_min_bytes;/* sum over launches of the compulsory bytes: tree once,      */
                             /*   referenced factor rows once, output once */
+  int32_t  exchange;        /* SPLATT_XCHG_* the call's factor-row exchange ran as (0 on   */
+                            /*   one rank)                                                  */
 } splatt_stats;
 
 /* ---------------------------------------------------------------- context */
@@ -167,6 +169,28 @@ splatt_status splatt_ctx_set_comm(splatt_ctx* ctx, const void* id128, int nranks
  * Errors: BADINPUT (unknown mode).                                                       */
 enum { SPLATT_PART_SLICES = 0, SPLATT_PART_NNZ = 1, SPLATT_PART_AUTO = 2 };
 splatt_status splatt_ctx_set_partition(splatt_ctx* ctx, int32_t mode);
+
+/* How a sharded context shares each mode's solved factor rows (SURVEY.md §8(e) step 5,
+ * "updated factor rows are shared"; PAPER.md:212-213, :606 distributed SPLATT):
+ *   COLLECTIVE (default): after the row solve, an all-gather of the owned row ranges (NCCL
+ *           grouped broadcasts), serialised behind the solve kernel.
+ *   PEER:   the row-solve kernel itself stores every solved row at the same offset of every
+ *           peer's factor matrix (peer-to-peer stores over NVLink / NVSwitch from inside the
+ *           kernel: the transfer overlaps the solve slab by slab and no separate all-gather
+ *           runs).  The factor matrices then live in one cudaMalloc slab per context, mapped
+ *           into the peers once per call with CUDA IPC handles (exchanged with one small NCCL
+ *           all-gather, which is also the barrier between the factor initialisation and the
+ *           first remote store).  Ordering: a kernel's peer stores are complete when it
+ *           completes; the statistics all-reduce that follows every solve cannot finish on
+ *           any rank before every rank's solve has finished, so a rank reads remote rows only
+ *           after they landed, and a rank's next store into a matrix happens only after every
+ *           peer has passed the all-reduce behind its last reader of it.  Needs <= 8 ranks on
+ *           one node with peer access; if any rank cannot map a peer, every rank falls back
+ *           to COLLECTIVE for the call (splatt_stats.exchange tells which ran).  Results are
+ *           bit-identical to COLLECTIVE.
+ * Errors: BADINPUT (unknown mode).                                                       */
+enum { SPLATT_XCHG_COLLECTIVE = 0, SPLATT_XCHG_PEER = 1 };
+splatt_status splatt_ctx_set_exchange(splatt_ctx* ctx, int32_t mode);
 
 /* In-process loopback group (testing/emulation of the sharded path on ONE device): nranks
  * logical ranks, each a host thread with its own context and its own stream (a context

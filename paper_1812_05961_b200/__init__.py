@@ -77,7 +77,8 @@ class Stats(C.Structure):
                 ("iters", C.c_int32), ("nranks", C.c_int32), ("t_call", C.c_double),
                 ("t_host_sync", C.c_double), ("host_syncs", C.c_int32),
                 ("t_aux_inverse", C.c_double), ("t_aux_fit", C.c_double),
-                ("mttkrp_min_bytes", C.c_double)]
+                ("mttkrp_min_bytes", C.c_double),
+                ("exchange", C.c_int32)]
 
     def to_dict(self, nmodes=None):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "csf_nodes"}
@@ -128,6 +129,7 @@ def lib():
                 "splatt_partition": (st, [P, u64, i32, P]),
                 "splatt_partition_nnz": (st, [P, u64, i32, i32, P, P, P, P]),
                 "splatt_ctx_set_partition": (st, [P, i32]),
+                "splatt_ctx_set_exchange": (st, [P, i32]),
                 "splatt_ctx_set_leaf_tiling": (st, [P, f64]),
                 "splatt_ctx_set_deterministic": (st, [P, i32]),
                 "splatt_csf_build": (st, [P, C.POINTER(Coo), i32, P, i32, C.POINTER(P)]),
@@ -233,6 +235,13 @@ class Context:
         C-14 cut), "nnz" (P2, equal nonzero ranges, split slices exchanged) or "auto"
         (per mode, P2 where P1's imbalance is large; the default)."""
         _raise(lib().splatt_ctx_set_partition(self._p, {"slices": 0, "nnz": 1, "auto": 2}[mode]),
+               self._p)
+
+    def set_exchange(self, mode: str = "collective"):
+        """How a sharded context shares solved factor rows: "collective" (NCCL all-gather
+        after the solve; the default) or "peer" (the solve kernel stores its rows straight
+        into the peers' factor matrices over NVLink; <= 8 ranks of one node)."""
+        _raise(lib().splatt_ctx_set_exchange(self._p, {"collective": 0, "peer": 1}[mode]),
                self._p)
 
     def set_deterministic(self, on: bool = True):

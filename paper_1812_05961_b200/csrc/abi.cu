@@ -231,6 +231,13 @@ splatt_status splatt_ctx_set_partition(splatt_ctx* ctx, int32_t mode) {
   return SPLATT_OK;
 }
 
+splatt_status splatt_ctx_set_exchange(splatt_ctx* ctx, int32_t mode) {
+  if (!ctx || (mode != SPLATT_XCHG_COLLECTIVE && mode != SPLATT_XCHG_PEER))
+    return SPLATT_ERR_BADINPUT;
+  ctx->exchange = mode;
+  return SPLATT_OK;
+}
+
 splatt_status splatt_partition_nnz(const uint64_t* w, uint64_t S, int32_t G, int32_t rank,
                                    uint64_t* row_bounds, uint64_t* split, uint64_t* nsplit,
                                    splatt_nnz_share* share) {

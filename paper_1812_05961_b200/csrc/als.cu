@@ -410,8 +410,26 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   // -------------------------------------------------------------- factors
   std::vector<DevBuf<double>> A(N);
   uint64_t maxI = 0, base = 0;
+  // SPLATT_XCHG_PEER: the factors live in the context's cudaMalloc slab (one IPC handle maps
+  // all of them into the peers), at offsets every rank computes alike.
+  // (also with a one-rank communicator: no peers, but the mapping exchange runs)
+  const bool want_peer = sharded && G <= kMaxPeerRanks && ctx->exchange == SPLATT_XCHG_PEER;
+  size_t slab_off[SPLATT_MAX_NMODES + 1] = {0};
+  for (int n = 0; n < N; ++n)
+    slab_off[n + 1] = slab_off[n] + ((X.dims[n] * ld * sizeof(double) + 255) & ~(size_t)255);
+  if (want_peer && slab_off[N] > ctx->peer_slab_cap) {
+    // (every remote store into the old slab landed before the previous call returned: its
+    // last solve was followed by an all-reduce on every rank)
+    if (ctx->peer_slab) SB_CUDA(cudaFree(ctx->peer_slab));
+    ctx->peer_slab = nullptr;
+    ctx->peer_slab_cap = 0;
+    SB_CUDA(cudaMalloc((void**)&ctx->peer_slab, slab_off[N]));
+    ctx->peer_slab_cap = slab_off[N];
+    ++ctx->peer_slab_gen;
+  }
   for (int n = 0; n < N; ++n) {
-    A[n].alloc(X.dims[n] * ld, s);
+    if (want_peer) A[n].adopt(reinterpret_cast<double*>(ctx->peer_slab + slab_off[n]), X.dims[n] * ld);
+    else A[n].alloc(X.dims[n] * ld, s);
     maxI = std::max(maxI, X.dims[n]);
     if (init) {
       SB_CUDA(cudaMemsetAsync(A[n].p, 0, X.dims[n] * ld * sizeof(double), s));
@@ -445,6 +463,26 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     gram_from_stats(ctx, stats.p, R, Gall.p + n * RR);
   }
   tm.end();
+
+  // Peer exchange: map the slabs after the factor initialisation and the initial Grams are
+  // enqueued (the exchange of handles is stream-ordered behind them on every rank: no rank
+  // stores into a peer's matrix before the peer has initialised and read it).
+  PeerRows peer_rows[SPLATT_MAX_NMODES] = {};
+  bool peer_x = false;
+  if (want_peer) {
+    void* bases[kMaxPeerRanks] = {nullptr};
+    tm.begin(kComm);
+    // (the slab's capacity, not this call's extent: it is what the handle covers, and
+    // ranks given the same tensor hold the same capacity)
+    peer_x = ctx->comm->map_peers(ctx->peer_slab, ctx->peer_slab_cap, ctx->peer_slab_gen, s, bases);
+    ++ctx->host_syncs;
+    tm.end();
+    for (int n = 0; n < N && peer_x; ++n)
+      for (int g = 0; g < G; ++g)
+        if (g != me)
+          peer_rows[n].p[peer_rows[n].n++] =
+              reinterpret_cast<double*>(static_cast<char*>(bases[g]) + slab_off[n]);
+  }
 
   // ----------------------------------------------------------------- loop
   DevBuf<double> rpart(rows_partials_cap(ctx, R), s);  // per-CTA solve partials (RowsReduce)
@@ -602,13 +640,15 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       tm.begin(kInverse);
       rows_solve_stats(ctx, M.p, A[n].p, lo, hi, R, ld, Vinv.p, tau.p, true, n == N - 1,
                        status.p, stats.p, sharded ? nullptr : &lo_fused,
-                       sharded ? nullptr : &rr);
+                       sharded ? nullptr : &rr, peer_x ? &peer_rows[n] : nullptr);
       tm.end();
       if (sharded) {
         tm.begin(kComm);
         ctx->comm->allreduce_sum(stats.p, stats_sum_len(R), s);
         ctx->comm->allreduce_max(stats.p + stats_max_off(R), R, s);
-        ctx->comm->allgatherv_rows(A[n].p, bounds[n], ld, s);
+        // (peer exchange: the solve already stored the rows on every rank, and the
+        // all-reduces above cannot complete before every rank's solve has)
+        if (!peer_x) ctx->comm->allgatherv_rows(A[n].p, bounds[n], ld, s);
         tm.end();
         tm.begin(kNorm);
         lambda_gram(ctx, stats.p, R, it == 1, lambda.p, Gall.p + n * RR, inner.p,
@@ -731,6 +771,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       for (int l = 0; l < N; ++l) st->csf_nodes[k][l] = csf[k]->nodes[l];
     st->iters = it_done;
     st->nranks = G;
+    st->exchange = peer_x ? SPLATT_XCHG_PEER : SPLATT_XCHG_COLLECTIVE;
     st->t_call = call_ms * 1e-3;
     st->host_syncs = (int32_t)(ctx->host_syncs - syncs0);
     st->t_host_sync = ctx->host_sync_s - sync_s0;

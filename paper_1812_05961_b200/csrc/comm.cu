@@ -8,6 +8,9 @@
 // (NCCL has no allgatherv).  All on the context stream, so they order with kernels.
 #include <dlfcn.h>
 #include <nccl.h>
+#include <unistd.h>
+
+#include <cstring>
 
 #include <mutex>
 
@@ -25,6 +28,8 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
@@ -47,6 +52,7 @@ NcclApi& api() {
     SB_SYM(CommDestroy, "ncclCommDestroy");
     SB_SYM(AllReduce, "ncclAllReduce");
     SB_SYM(Broadcast, "ncclBroadcast");
+    SB_SYM(AllGather, "ncclAllGather");
     SB_SYM(GroupStart, "ncclGroupStart");
     SB_SYM(GroupEnd, "ncclGroupEnd");
     SB_SYM(GetErrorString, "ncclGetErrorString");
@@ -65,10 +71,84 @@ void check(ncclResult_t r, const char* what) {
   }
 }
 
+// What a rank publishes about its factor slab (SPLATT_XCHG_PEER): the CUDA IPC handle of
+// the cudaMalloc allocation, its size, the owner's allocation generation (a new allocation
+// at a recycled address must not be taken for the old one) and the owner's process id.
+struct SlabRec {
+  cudaIpcMemHandle_t handle;
+  uint64_t bytes, gen;
+  int64_t pid;
+  int32_t ok;
+  int32_t pad;
+};
+
 struct NcclComm final : Comm {
   ncclComm_t comm = nullptr;
+  // peers' slabs mapped into this process, reused while the owner keeps its allocation
+  struct Mapping {
+    SlabRec rec{};
+    void* ptr = nullptr;
+  };
+  std::vector<Mapping> maps;
+  void close_map(Mapping& m) {
+    if (m.ptr && cudaIpcCloseMemHandle(m.ptr) != cudaSuccess) cudaGetLastError();
+    m.ptr = nullptr;
+  }
   ~NcclComm() override {
+    for (Mapping& m : maps) close_map(m);
     if (comm && api().CommDestroy) api().CommDestroy(comm);
+  }
+  // Handles travel with one all-gather of SlabRec bytes; a second tiny all-reduce(max) of
+  // the ranks' failure flags makes the outcome the same everywhere.  Two host syncs per call.
+  bool map_peers(void* base, size_t bytes, uint64_t gen, cudaStream_t s, void** peers) override {
+    if (nranks > kMaxPeerRanks || !api().AllGather) return false;  // same answer on every rank
+    maps.resize(nranks);
+    const size_t rec = sizeof(SlabRec);
+    std::vector<SlabRec> all(nranks);
+    SlabRec mine{};
+    mine.bytes = bytes;
+    mine.gen = gen;
+    mine.pid = (int64_t)getpid();
+    mine.ok = cudaIpcGetMemHandle(&mine.handle, base) == cudaSuccess ? 1 : 0;
+    if (!mine.ok) cudaGetLastError();
+    DevBuf<char> d((size_t)nranks * rec, s);
+    DevBuf<double> flag(1, s);
+    SB_CUDA(cudaMemcpyAsync(d.p + (size_t)rank * rec, &mine, rec, cudaMemcpyHostToDevice, s));
+    check(api().AllGather(d.p + (size_t)rank * rec, d.p, rec, ncclChar, comm, s), "ncclAllGather");
+    SB_CUDA(cudaMemcpyAsync(all.data(), d.p, (size_t)nranks * rec, cudaMemcpyDeviceToHost, s));
+    SB_CUDA(cudaStreamSynchronize(s));
+    double failed = mine.ok ? 0.0 : 1.0;
+    for (int g = 0; g < nranks; ++g) {
+      if (g == rank) {
+        peers[g] = base;
+        continue;
+      }
+      Mapping& m = maps[g];
+      const SlabRec& r = all[g];
+      if (!r.ok || r.bytes != bytes || r.pid == mine.pid) {  // IPC needs another process
+        failed = 1.0;
+        continue;
+      }
+      const bool same = m.ptr && m.rec.gen == r.gen && m.rec.pid == r.pid &&
+                        m.rec.bytes == r.bytes &&
+                        memcmp(&m.rec.handle, &r.handle, sizeof(r.handle)) == 0;
+      if (!same) {
+        close_map(m);
+        if (cudaIpcOpenMemHandle(&m.ptr, r.handle, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+          cudaGetLastError();
+          m.ptr = nullptr;
+          failed = 1.0;
+          continue;
+        }
+        m.rec = r;
+      }
+      peers[g] = m.ptr;
+    }
+    SB_CUDA(cudaMemcpyAsync(flag.p, &failed, sizeof(double), cudaMemcpyHostToDevice, s));
+    allreduce_max(flag.p, 1, s);
+    SB_CUDA(cudaMemcpyAsync(&failed, flag.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    SB_CUDA(cudaStreamSynchronize(s));
+    return failed == 0.0;
   }
   void allreduce_sum(double* buf, size_t n, cudaStream_t s) override {
     check(api().AllReduce(buf, buf, n, ncclFloat64, ncclSum, comm, s), "ncclAllReduce(sum)");

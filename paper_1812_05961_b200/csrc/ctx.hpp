@@ -26,7 +26,18 @@ struct Comm {
   // afterwards every rank holds all rows.
   virtual void allgatherv_rows(double* base, const std::vector<uint64_t>& bounds, int ld,
                                cudaStream_t s) = 0;
+  // SPLATT_XCHG_PEER: make the `bytes`-long cudaMalloc allocation starting at `base`
+  // (generation `gen`: bumped by the owner whenever it reallocates) addressable by every
+  // rank; peers[g] = rank g's allocation as seen from this device (peers[rank] = base).
+  // Collective, stream-ordered behind the work already enqueued on `s` on every rank and
+  // complete on return (it is the barrier between the factor initialisation and the first
+  // remote store).  Returns false on EVERY rank if any rank could not map some peer.
+  virtual bool map_peers(void* base, size_t bytes, uint64_t gen, cudaStream_t s, void** peers) {
+    (void)base; (void)bytes; (void)gen; (void)s; (void)peers;
+    return false;
+  }
 };
+constexpr int kMaxPeerRanks = 8;  // SPLATT_XCHG_PEER: ranks whose factor copies a solve stores to
 
 std::unique_ptr<Comm> make_nccl_comm(const void* id128, int nranks, int rank);
 std::unique_ptr<Comm> make_loopback_comm(splatt_loopback* group, int rank);
@@ -42,6 +53,12 @@ struct splatt_ctx {
   std::string err;
   uint64_t kernel_launches = 0;
   int part_mode = SPLATT_PART_AUTO;    // sharded path: P1 / P2 per mode (SPLATT_PART_*)
+  int exchange = SPLATT_XCHG_COLLECTIVE;  // sharded path: how solved rows reach the peers
+  // SPLATT_XCHG_PEER: the factor matrices of a sharded call live in this cudaMalloc slab
+  // (IPC handles need a whole allocation), kept across calls and grown on demand.
+  char* peer_slab = nullptr;
+  size_t peer_slab_cap = 0;
+  uint64_t peer_slab_gen = 0;
   double leaf_tile_frac = -1.0;        // ROOT MTTKRP leaf tiling (0 = off, < 0 = auto)
   bool deterministic = false;          // ROOT MTTKRP seams: fixed-order sums, no atomics
   // While a cpd_als call builds trees that only run ROOT traversals (policy ALL): the padded
@@ -91,6 +108,8 @@ struct splatt_ctx {
     return h_pinned;
   }
   ~splatt_ctx() {
+    comm.reset();  // closes its mappings of the peers' slabs before ours goes
+    if (peer_slab) cudaFree(peer_slab);
     if (h_pinned) cudaFreeHost(h_pinned);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_pool_aux) cudaEventDestroy(e);
@@ -236,6 +255,12 @@ struct DevBuf {
     return *this;
   }
   T* get() const { return p; }
+  // Non-owning view of memory someone else frees.
+  void adopt(T* ptr, size_t count) {
+    release();
+    p = ptr;
+    n = count;
+  }
 };
 
 // Spans of CUDA events recorded on one stream, read once at the end.  Events come from a

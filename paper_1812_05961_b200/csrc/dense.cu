@@ -203,6 +203,7 @@ struct RowsArgs {
   const int* conv;  // ALS converged: skip (splatt_ctx::d_conv)
   double* part;  // gridDim.x x stats_len(R)
   bool solve;
+  PeerRows peers;  // n = 0: none
 };
 
 #ifndef SB_SOLVE_RPG
@@ -342,8 +343,12 @@ __global__ void __launch_bounds__(BT, kMaxBP == 1 ? (BT == 128 ? 4 : 2) : 1)
       }
       __syncthreads();
       double2* dst = reinterpret_cast<double2*>(a.A + row0 * ld);
-      for (int e = threadIdx.x; e < nrows * half; e += blockDim.x)
-        dst[e] = *reinterpret_cast<const double2*>(tile + (e / half) * ldp + 2 * (e % half));
+      for (int e = threadIdx.x; e < nrows * half; e += blockDim.x) {
+        const double2 v = *reinterpret_cast<const double2*>(tile + (e / half) * ldp + 2 * (e % half));
+        dst[e] = v;
+        for (int q = 0; q < a.peers.n; ++q)  // fused all-gather: the peers' copies of the row
+          reinterpret_cast<double2*>(a.peers.p[q] + row0 * ld)[e] = v;
+      }
     }
 #pragma unroll
     for (int k = 0; k < kMaxBP; ++k) {
@@ -533,8 +538,12 @@ __global__ void __launch_bounds__(W * 32, mma_minb(NT)) solve_gram_mma_kernel(co
         *reinterpret_cast<double2*>(buf + g * LDP + n * 8 + 2 * t) = make_double2(c[n][0], c[n][1]);
       __syncwarp();
       double2* dst = reinterpret_cast<double2*>(a.A + row0 * ld);
-      for (int e = lane; e < nrows * half; e += 32)
-        dst[e] = *reinterpret_cast<const double2*>(buf + (e / half) * LDP + 2 * (e % half));
+      for (int e = lane; e < nrows * half; e += 32) {
+        const double2 v = *reinterpret_cast<const double2*>(buf + (e / half) * LDP + 2 * (e % half));
+        dst[e] = v;
+        for (int q = 0; q < a.peers.n; ++q)  // fused all-gather: the peers' copies of the row
+          reinterpret_cast<double2*>(a.peers.p[q] + row0 * ld)[e] = v;
+      }
     } else {
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
@@ -869,7 +878,7 @@ bool getenv_flag(const char* name) {
 void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, uint64_t hi,
                       int R, int ld, const double* Vinv, const double* tau, bool solve,
                       bool inner, const int* status, double* stats, const LambdaOut* fuse,
-                      const RowsReduce* rr) {
+                      const RowsReduce* rr, const PeerRows* peers) {
   // Vinv: ld x ld, zero pads (hadamard_inverse)
   (void)inner;  // the inner product is always produced by the solve (it is free)
   const size_t SL = stats_len(R);
@@ -924,6 +933,7 @@ void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, 
   a.status = status;
   a.conv = ctx->d_conv;
   a.solve = solve;
+  if (peers && solve) a.peers = *peers;
 #ifndef SB_SOLVE_MAX_PER_SM
 #define SB_SOLVE_MAX_PER_SM 3
 #endif

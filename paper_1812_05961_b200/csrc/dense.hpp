@@ -60,10 +60,18 @@ struct RowsReduce {
   EventTimer* tm;  // optional span on rr->stream
   int cat;
 };
+// peers (SPLATT_XCHG_PEER, splatt_b200.h): the other ranks' copies of A; every solved row is
+// also stored at the same offset of each (the all-gather of §8(e) step 5 fused into the
+// solve: remote stores from inside the kernel, slab by slab).
+struct PeerRows {
+  double* p[kMaxPeerRanks - 1];
+  int n;
+};
 void rows_solve_stats(splatt_ctx* ctx, const double* M, double* A, uint64_t lo, uint64_t hi,
                       int R, int ld, const double* Vinv, const double* tau, bool solve,
                       bool inner, const int* status, double* stats,
-                      const LambdaOut* fuse = nullptr, const RowsReduce* rr = nullptr);
+                      const LambdaOut* fuse = nullptr, const RowsReduce* rr = nullptr,
+                      const PeerRows* peers = nullptr);
 size_t rows_partials_cap(splatt_ctx* ctx, int R);
 
 // a8 + a9: lambda (first: 2-norm = sqrt(G~_rr); else max(1, colmax)), G_n =

@@ -88,6 +88,16 @@ struct LoopbackComm final : Comm {
     SB_CUDA(cudaStreamSynchronize(s));
     sync_ranks();  // nobody overwrites its rows while a peer still copies them
   }
+  // One device, one address space: the peers' slabs are addressable as they are.
+  bool map_peers(void* base, size_t bytes, uint64_t gen, cudaStream_t s, void** peers) override {
+    (void)bytes; (void)gen;
+    SB_CUDA(cudaStreamSynchronize(s));  // this rank's factor initialisation is done
+    grp->ptrs[rank] = base;
+    sync_ranks();
+    for (int g = 0; g < nranks; ++g) peers[g] = const_cast<void*>(grp->ptrs[g]);
+    sync_ranks();  // every rank has read the table before a later exchange reuses it
+    return true;
+  }
 };
 
 }  // namespace

@@ -26,7 +26,8 @@ def sb(cuda_ok):
     return m
 
 
-def run_ranks(sb, t, G, R, iters, seed, tol=0.0, partition="slices"):
+def run_ranks(sb, t, G, R, iters, seed, tol=0.0, partition="slices", exchange="collective",
+              calls=1):
     import torch
     grp = sb.Loopback(G)
     results, errors = [None] * G, []
@@ -37,12 +38,14 @@ def run_ranks(sb, t, G, R, iters, seed, tol=0.0, partition="slices"):
             ctx = sb.Context(0, stream=stream)
             ctx.set_comm_loopback(grp, r)
             ctx.set_partition(partition)
+            ctx.set_exchange(exchange)
             with torch.cuda.stream(stream):
                 ind = [torch.from_numpy(a.view(np.int32)).cuda() for a in t.ind]
                 vals = torch.from_numpy(t.vals).cuda()
             stream.synchronize()
-            res = sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=iters, tol=tol, seed=seed,
-                             ctx=ctx, out_device=False, stats=True)
+            for _ in range(calls):  # repeated calls reuse the context's arenas / factor slab
+                res = sb.cpd_als(ind, vals, t.dims, rank=R, max_iters=iters, tol=tol, seed=seed,
+                                 ctx=ctx, out_device=False, stats=True)
             results[r] = res
             ctx.close()
         except Exception as e:  # pragma: no cover
@@ -169,3 +172,102 @@ def test_auto_partition_picks_p2_for_heavy_mode(sb):
         assert abs(multi[r]["fit"] - ref["fit"]) <= ALS_TOL * abs(ref["fit"])
     loc0 = [multi[r]["stats"]["csf_nodes"][0][2] for r in range(4)]
     assert sum(loc0) == t.nnz and max(loc0) - min(loc0) <= 1  # mode 0: P2
+
+
+# ---- SPLATT_XCHG_PEER: the row solve stores its rows straight into the peers' factor
+# matrices (splatt_b200.h, splatt_ctx_set_exchange); the all-gather never runs.  The model must
+# be bit-identical to the collective exchange on every rank (the same values are stored) and
+# match the oracle.
+
+@pytest.mark.parametrize("partition", ["slices", "nnz"])
+@pytest.mark.parametrize("G,R", [(2, 16), (3, 35), (8, 16), (4, 80)])  # R = 80: the FMA-pipe solve
+def test_peer_exchange_bit_identical_to_collective(sb, G, R, partition):
+    t = synth.generate((4000, 1100, 7500), 150_000, [("zipf", 1.1)] * 3, "ratings", seed=22)
+    iters = 4
+    coll = run_ranks(sb, t, G, R, iters, seed=5, partition=partition)
+    peer = run_ranks(sb, t, G, R, iters, seed=5, partition=partition, exchange="peer", calls=2)
+    ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=R, max_iters=iters, seed=5)
+    for r in range(G):
+        assert coll[r]["stats"]["exchange"] == 0 and peer[r]["stats"]["exchange"] == 1
+        for n in range(3):
+            assert np.array_equal(peer[r]["factors"][n], coll[r]["factors"][n])
+            assert rel_fro(peer[r]["factors"][n], ref["factors"][n]) <= ALS_TOL
+        assert np.array_equal(peer[r]["lam"], coll[r]["lam"])
+        assert peer[r]["fit"] == coll[r]["fit"]
+        assert abs(peer[r]["fit"] - ref["fit"]) <= ALS_TOL * abs(ref["fit"])
+
+
+def test_peer_exchange_four_modes_empty_ranks_and_growth(sb):
+    """4-mode trees (second-generation ROOT kernel), ranks that own no rows of the last mode,
+    and a context whose factor slab grows between calls (a small tensor first)."""
+    import torch
+    small = synth.generate((60, 50, 40, 3), 2_000, [("zipf", 1.05)] * 4, "u01", seed=8)
+    t = synth.generate((300, 200, 100, 3), 20_000, [("zipf", 1.05)] * 4, "u01", seed=9)
+    G, R = 4, 8
+    grp = sb.Loopback(G)
+    results, errors = [None] * G, []
+
+    def worker(r):
+        try:
+            stream = torch.cuda.Stream(0)
+            ctx = sb.Context(0, stream=stream)
+            ctx.set_comm_loopback(grp, r)
+            ctx.set_exchange("peer")
+            out = []
+            for x in (small, t):
+                with torch.cuda.stream(stream):
+                    ind = [torch.from_numpy(a.view(np.int32)).cuda() for a in x.ind]
+                    vals = torch.from_numpy(x.vals).cuda()
+                stream.synchronize()
+                out.append(sb.cpd_als(ind, vals, x.dims, rank=R, max_iters=3, seed=2, ctx=ctx,
+                                      out_device=False, stats=True))
+            results[r] = out
+            ctx.close()
+        except Exception as e:  # pragma: no cover
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(G)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(timeout=600)
+    grp.close()
+    assert not errors, errors
+    for k, x in enumerate((small, t)):
+        ref = oracle.cpd_als(x.dims, x.ind, x.vals, rank=R, max_iters=3, seed=2)
+        for r in range(G):
+            assert results[r][k]["stats"]["exchange"] == 1
+            for n in range(4):
+                assert rel_fro(results[r][k]["factors"][n], ref["factors"][n]) <= ALS_TOL
+            assert abs(results[r][k]["fit"] - ref["fit"]) <= ALS_TOL * abs(ref["fit"])
+
+
+def test_peer_exchange_tol_stop(sb):
+    t = synth.generate_config("c1")
+    multi = run_ranks(sb, t, 2, 8, 100, seed=1, tol=1e-4, exchange="peer")
+    ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=8, max_iters=100, tol=1e-4, seed=1)
+    for r in range(2):
+        assert multi[r]["iters"] == ref["iters"]
+        assert abs(multi[r]["fit"] - ref["fit"]) <= ALS_TOL * abs(ref["fit"])
+
+
+def test_peer_exchange_one_rank_nccl(sb):
+    """A one-rank NCCL communicator: no peer to store to, but the mapping exchange runs for
+    real (cudaIpcGetMemHandle on the factor slab, ncclAllGather of the handle records, the
+    failure-flag all-reduce); the model is the oracle's."""
+    import torch
+    t = synth.generate((400, 300, 200), 20_000, [("zipf", 1.1)] * 3, "ratings", seed=3)
+    ref = oracle.cpd_als(t.dims, t.ind, t.vals, rank=8, max_iters=3, seed=5)
+    stream = torch.cuda.Stream(0)
+    ctx = sb.Context(0, stream=stream)
+    ctx.set_comm(single=True)
+    ctx.set_exchange("peer")
+    with torch.cuda.stream(stream):
+        ind = [torch.from_numpy(a.view(np.int32)).cuda() for a in t.ind]
+        vals = torch.from_numpy(t.vals).cuda()
+    stream.synchronize()
+    res = sb.cpd_als(ind, vals, t.dims, rank=8, max_iters=3, seed=5, ctx=ctx, out_device=False,
+                     stats=True)
+    assert res["stats"]["exchange"] == 1 and res["stats"]["nranks"] == 1
+    for n in range(3):
+        assert rel_fro(res["factors"][n], ref["factors"][n]) <= ALS_TOL
