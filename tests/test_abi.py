@@ -75,6 +75,20 @@ def test_bad_args_return_status_without_device(L):
     assert L.splatt_partition(None, 0, 0, None) == -1
     assert L.splatt_mttkrp_csf(None, None, 0, 0, None, 1, 1, None) == -1
     assert L.splatt_csf_dispatch(None, 0, None, None, None) == -1
+    assert L.splatt_ctx_set_exchange(None, 0) == -1
+    assert L.splatt_ctx_set_partition(None, 0) == -1
+
+
+def test_exchange_constants_match_header_and_binding():
+    txt = open(HEADER).read()
+    assert re.search(r"SPLATT_XCHG_COLLECTIVE\s*=\s*0\b", txt)
+    assert re.search(r"SPLATT_XCHG_PEER\s*=\s*1\b", txt)
+    src = open(os.path.join(ROOT, "paper_1812_05961_b200", "__init__.py")).read()
+    assert '{"collective": 0, "peer": 1}' in src
+    # the statistics struct ends with the exchange word in both the header and the binding
+    assert re.search(r"int32_t\s+exchange;[^}]*}\s*splatt_stats;", txt, re.S)
+    import paper_1812_05961_b200 as sb
+    assert sb.Stats._fields_[-1][0] == "exchange"
 
 
 def test_policy_constants_match_header():
