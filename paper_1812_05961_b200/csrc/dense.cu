@@ -343,11 +343,12 @@ __global__ void __launch_bounds__(BT, kMaxBP == 1 ? (BT == 128 ? 4 : 2) : 1)
       }
       __syncthreads();
       double2* dst = reinterpret_cast<double2*>(a.A + row0 * ld);
-      for (int e = threadIdx.x; e < nrows * half; e += blockDim.x) {
-        const double2 v = *reinterpret_cast<const double2*>(tile + (e / half) * ldp + 2 * (e % half));
-        dst[e] = v;
-        for (int q = 0; q < a.peers.n; ++q)  // fused all-gather: the peers' copies of the row
-          reinterpret_cast<double2*>(a.peers.p[q] + row0 * ld)[e] = v;
+      for (int e = threadIdx.x; e < nrows * half; e += blockDim.x)
+        dst[e] = *reinterpret_cast<const double2*>(tile + (e / half) * ldp + 2 * (e % half));
+      for (int q = 0; q < a.peers.n; ++q) {  // fused all-gather: the peers' copies of the rows
+        double2* pd = reinterpret_cast<double2*>(a.peers.p[q] + row0 * ld);
+        for (int e = threadIdx.x; e < nrows * half; e += blockDim.x)
+          pd[e] = *reinterpret_cast<const double2*>(tile + (e / half) * ldp + 2 * (e % half));
       }
     }
 #pragma unroll
@@ -538,11 +539,12 @@ __global__ void __launch_bounds__(W * 32, mma_minb(NT)) solve_gram_mma_kernel(co
         *reinterpret_cast<double2*>(buf + g * LDP + n * 8 + 2 * t) = make_double2(c[n][0], c[n][1]);
       __syncwarp();
       double2* dst = reinterpret_cast<double2*>(a.A + row0 * ld);
-      for (int e = lane; e < nrows * half; e += 32) {
-        const double2 v = *reinterpret_cast<const double2*>(buf + (e / half) * LDP + 2 * (e % half));
-        dst[e] = v;
-        for (int q = 0; q < a.peers.n; ++q)  // fused all-gather: the peers' copies of the row
-          reinterpret_cast<double2*>(a.peers.p[q] + row0 * ld)[e] = v;
+      for (int e = lane; e < nrows * half; e += 32)
+        dst[e] = *reinterpret_cast<const double2*>(buf + (e / half) * LDP + 2 * (e % half));
+      for (int q = 0; q < a.peers.n; ++q) {  // fused all-gather: the peers' copies of the rows
+        double2* pd = reinterpret_cast<double2*>(a.peers.p[q] + row0 * ld);
+        for (int e = lane; e < nrows * half; e += 32)
+          pd[e] = *reinterpret_cast<const double2*>(buf + (e / half) * LDP + 2 * (e % half));
       }
     } else {
 #pragma unroll
