@@ -2,7 +2,10 @@
 # reference arm, ROOT MTTKRP DRAM traffic (c5, c3, c2), the c5 launch list, one full ncu capture.
 mkdir -p gpurun_out
 P=${P:-fin}
-timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/${P}_gpu_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/${P}_gpu_pytest.log
+# SKIP_TESTS=1: the GPU test log comes from a separate call of the same tree
+if [ -z "$SKIP_TESTS" ]; then
+timeout 1500 python -m pytest tests -x -q -m gpu --durations=25 > gpurun_out/${P}_gpu_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/${P}_gpu_pytest.log
+fi
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${P}_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/${P}_smoke.log
 python bench.py > gpurun_out/${P}_bench_c5.json 2> gpurun_out/${P}_bench_c5.err
 python bench.py --config c3 --no-cpu-baseline > gpurun_out/${P}_bench_c3.json 2> gpurun_out/${P}_bench_c3.err
