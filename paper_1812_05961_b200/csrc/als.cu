@@ -644,8 +644,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
       tm.end();
       if (sharded) {
         tm.begin(kComm);
-        ctx->comm->allreduce_sum(stats.p, stats_sum_len(R), s);
-        ctx->comm->allreduce_max(stats.p + stats_max_off(R), R, s);
+        ctx->comm->allreduce_stats(stats.p, stats_sum_len(R), (size_t)R, s);  // max part follows
         // (peer exchange: the solve already stored the rows on every rank, and the
         // all-reduces above cannot complete before every rank's solve has)
         if (!peer_x) ctx->comm->allgatherv_rows(A[n].p, bounds[n], ld, s);

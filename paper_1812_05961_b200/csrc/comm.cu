@@ -2,10 +2,12 @@
 //
 // libnccl.so.2 is dlopen'ed on first use (the one torch already loaded is picked up by
 // soname), so the library itself has no link-time NCCL dependency and loads on a
-// CPU-only host.  Exchange per mode (§8(e) steps 4-5): all-reduce(sum) of the R x R
-// partial Gram + fit inner product, all-reduce(max) of the column maxima, and an
-// all-gather of the owned factor rows with uneven counts as grouped broadcasts
-// (NCCL has no allgatherv).  All on the context stream, so they order with kernels.
+// CPU-only host.  Exchange per mode (§8(e) steps 4-5): the R x R partial Gram + fit inner
+// product (summed) and the column maxima (maximised) in one all-gather of the ranks'
+// statistics followed by a rank-ordered local reduction (allreduce_stats), and an
+// all-gather of the owned factor rows with uneven counts as grouped broadcasts (NCCL has no
+// allgatherv) unless the solve kernel already stored them into the peers (map_peers,
+// SPLATT_XCHG_PEER).  All on the context stream, so they order with kernels.
 #include <dlfcn.h>
 #include <nccl.h>
 #include <unistd.h>
@@ -82,6 +84,21 @@ struct SlabRec {
   int32_t pad;
 };
 
+// out[i] = sum (i < nsum) or max (else) over the G gathered copies g[r * len + i], in rank
+// order: every rank computes the same bits, whatever algorithm NCCL picked for the gather.
+__global__ void gathered_reduce_kernel(const double* __restrict__ g, int G, size_t len,
+                                       size_t nsum, double* __restrict__ out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < len;
+       i += (size_t)gridDim.x * blockDim.x) {
+    double acc = g[i];
+    for (int r = 1; r < G; ++r) {
+      const double v = g[(size_t)r * len + i];
+      acc = i < nsum ? acc + v : fmax(acc, v);
+    }
+    out[i] = acc;
+  }
+}
+
 struct NcclComm final : Comm {
   ncclComm_t comm = nullptr;
   // peers' slabs mapped into this process, reused while the owner keeps its allocation
@@ -155,6 +172,17 @@ struct NcclComm final : Comm {
   }
   void allreduce_max(double* buf, size_t n, cudaStream_t s) override {
     check(api().AllReduce(buf, buf, n, ncclFloat64, ncclMax, comm, s), "ncclAllReduce(max)");
+  }
+  // One collective instead of two (the exchange is latency-bound: ~10 KB per rank): the
+  // ranks' statistics are all-gathered and every rank reduces them in rank order.
+  void allreduce_stats(double* buf, size_t nsum, size_t nmax, cudaStream_t s) override {
+    if (!api().AllGather) return Comm::allreduce_stats(buf, nsum, nmax, s);
+    const size_t len = nsum + nmax;
+    DevBuf<double> g((size_t)nranks * len, s);
+    check(api().AllGather(buf, g.p, len, ncclFloat64, comm, s), "ncclAllGather(stats)");
+    const unsigned blocks = (unsigned)std::min<size_t>(ceil_div(len, (size_t)256), 64);
+    gathered_reduce_kernel<<<std::max(1u, blocks), 256, 0, s>>>(g.p, nranks, len, nsum, buf);
+    SB_CUDA(cudaGetLastError());
   }
   void allgatherv_rows(double* base, const std::vector<uint64_t>& b, int ld,
                        cudaStream_t s) override {

@@ -22,6 +22,12 @@ struct Comm {
   virtual ~Comm() = default;
   virtual void allreduce_sum(double* buf, size_t n, cudaStream_t s) = 0;
   virtual void allreduce_max(double* buf, size_t n, cudaStream_t s) = 0;
+  // The per-mode statistics in one exchange: buf[0, nsum) summed and buf[nsum, nsum + nmax)
+  // maximised over the ranks, the same bits on every rank.
+  virtual void allreduce_stats(double* buf, size_t nsum, size_t nmax, cudaStream_t s) {
+    allreduce_sum(buf, nsum, s);
+    allreduce_max(buf + nsum, nmax, s);
+  }
   // Rows [bounds[g], bounds[g+1]) of the I x ld matrix `base` are valid on rank g;
   // afterwards every rank holds all rows.
   virtual void allgatherv_rows(double* base, const std::vector<uint64_t>& bounds, int ld,
