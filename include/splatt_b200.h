@@ -143,7 +143,8 @@ const char*   splatt_version(void);
  * every rank passes the same full COO; nonzeros are partitioned by
  * root slices of each mode's CSF (splatt_partition), each rank owns the output rows
  * of its slice range, updated factor rows are all-gathered and the R x R Grams,
- * column maxima and the fit inner product are all-reduced with NCCL.
+ * column maxima and the fit inner product are combined over the ranks with NCCL (one
+ * all-gather of the ranks' partials, reduced in rank order on every rank).
  * splatt_comm_unique_id: rank 0 only; writes 128 bytes (ncclUniqueId), to be
  * broadcast by the caller (e.g. torch.distributed).  splatt_ctx_set_comm: collective
  * over the nranks ranks (ncclCommInitRank).  NCCL is loaded at run time
@@ -181,10 +182,11 @@ splatt_status splatt_ctx_set_partition(splatt_ctx* ctx, int32_t mode);
  *           into the peers once per call with CUDA IPC handles (exchanged with one small NCCL
  *           all-gather, which is also the barrier between the factor initialisation and the
  *           first remote store).  Ordering: a kernel's peer stores are complete when it
- *           completes; the statistics all-reduce that follows every solve cannot finish on
- *           any rank before every rank's solve has finished, so a rank reads remote rows only
- *           after they landed, and a rank's next store into a matrix happens only after every
- *           peer has passed the all-reduce behind its last reader of it.  Needs <= 8 ranks on
+ *           completes; the statistics exchange (a collective every rank contributes to)
+ *           that follows every solve cannot finish on any rank before every rank's solve
+ *           has finished, so a rank reads remote rows only after they landed, and a rank's
+ *           next store into a matrix happens only after every peer has passed the exchange
+ *           behind its last reader of it.  Needs <= 8 ranks on
  *           one node with peer access; if any rank cannot map a peer, every rank falls back
  *           to COLLECTIVE for the call (splatt_stats.exchange tells which ran).  Results are
  *           bit-identical to COLLECTIVE.
