@@ -22,6 +22,8 @@ struct Comm {
   virtual ~Comm() = default;
   virtual void allreduce_sum(double* buf, size_t n, cudaStream_t s) = 0;
   virtual void allreduce_max(double* buf, size_t n, cudaStream_t s) = 0;
+  // Ranks that are threads on ONE device (loopback): device-wide settings are left alone.
+  virtual bool shares_device() const { return false; }
   // The per-mode statistics in one exchange: buf[0, nsum) summed and buf[nsum, nsum + nmax)
   // maximised over the ranks, the same bits on every rank.
   virtual void allreduce_stats(double* buf, size_t nsum, size_t nmax, cudaStream_t s) {

@@ -88,6 +88,7 @@ struct LoopbackComm final : Comm {
     SB_CUDA(cudaStreamSynchronize(s));
     sync_ranks();  // nobody overwrites its rows while a peer still copies them
   }
+  bool shares_device() const override { return true; }
   // One device, one address space: the peers' slabs are addressable as they are.
   bool map_peers(void* base, size_t bytes, uint64_t gen, cudaStream_t s, void** peers) override {
     (void)bytes; (void)gen;
