@@ -464,15 +464,12 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
   }
   tm.end();
 
-  // Factor matrices as a persisting L2 window for the loop (c5: 2.394 -> 2.325 ms per ROOT
-  // MTTKRP, step 235.6 -> 230.4 ms; profiles/ab_r02/l2p/): the tree records stream through L2 once per launch and otherwise evict rows that
-  // every launch gathers again.  Only when all factors fit the device's persisting set-aside
-  // and a third of L2 (a partly covered window is slower than none: its uncovered rows turn
-  // evict-first), and only around the loop: the CSF build needs the whole L2 (with a 40 MB
-  // set-aside left on, c5's build ran 41 -> 49 ms), so the set-aside is made after the build
-  // has finished on the device and removed when the call returns.  The limit is device-wide:
-  // not with loopback ranks sharing the device.  SPLATT_L2_PERSIST=0 turns it off, =<MB>
-  // forces the set-aside size.
+  // A/B knob, off by default (SPLATT_L2_PERSIST=<MB of set-aside>): the factor matrices as a
+  // persisting L2 window around the loop.  It showed that the streamed tree records evict
+  // gathered rows (c5: 2.394 -> 2.325 ms per launch); the kernels' evict-first hint on the
+  // record stream (root2.cuh, SB_ROOT2_EVICT) removes the cause instead (2.240 ms, the window
+  // adds nothing on top) without a device-wide limit, a host sync, or the set-aside's cost to
+  // the CSF build (profiles/ab_r02/l2p/, evict/).
   struct L2Window {
     cudaStream_t s = nullptr;
     bool on = false;
@@ -498,16 +495,8 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
     int maxwin = 0, maxpersist = 0;
     cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device);
     cudaDeviceGetAttribute(&maxpersist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
-    const size_t l2 = ctx->l2_bytes ? ctx->l2_bytes : ((size_t)126 << 20);
-    size_t aside = win + ((size_t)2 << 20);
-    bool want = max_iters >= 2 && win <= (size_t)maxwin && aside <= (size_t)maxpersist &&
-                aside <= l2 / 3 && !(ctx->comm && ctx->comm->shares_device());
-    // Measured per kernel: the second-generation ROOT kernel (4-mode trees, no_allocate
-    // gathers) gains 3%; the first-generation kernel's L1-allocating gathers lose 1.5% on
-    // c2 and tie on c4, so the window is for calls whose every mode runs the former.
-    for (int n = 0; n < N && want; ++n)
-      want = mode_level[n] == 0 && csf[mode_csf[n]]->nnz > 0 &&
-             root2_eligible(ctx, *csf[mode_csf[n]], ld);
+    size_t aside = 0;
+    bool want = false;
     if (e) {
       want = atoi(e) > 0 && win <= (size_t)maxwin;
       aside = (size_t)atoi(e) << 20;
@@ -530,7 +519,7 @@ void cpd_als_device(splatt_ctx* ctx, const DevCoo& X, int R, int max_iters, doub
         cudaGetLastError();
       }
     }
-    if (getenv("SPLATT_TRACE"))
+    if (e && getenv("SPLATT_TRACE"))
       fprintf(stderr, "[splatt] L2 persisting window: factors %zu bytes, set-aside %zu (max %d), %s\n",
               win, aside, maxpersist, l2win.on ? "on" : "off");
   }

@@ -99,14 +99,34 @@ __device__ __forceinline__ d4 ldg_row(const double* p) {
         : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
   return r;
 }
+// Leaf ids and values: read once per launch.  SB_STREAM_EVICT: with an L2 evict-first cache
+// hint, so the stream does not displace factor rows in L2 (A/B: profiles/ab_r02/evict/).
+#ifndef SB_STREAM_EVICT
+#define SB_STREAM_EVICT 0
+#endif
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));  // pure: hoistable
+  return pol;
+}
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
   uint32_t v;
+#if SB_STREAM_EVICT
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(v) : "l"(p), "l"(l2_evict_first_policy()));
+#else
   asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+#endif
   return v;
 }
 __device__ __forceinline__ double ld_stream_f64(const double* p) {
   double v;
+#if SB_STREAM_EVICT
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v) : "l"(p), "l"(l2_evict_first_policy()));
+#else
   asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+#endif
   return v;
 }
 __device__ __forceinline__ void st_row(double* p, const d4& v) {

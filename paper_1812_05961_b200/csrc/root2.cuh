@@ -184,6 +184,9 @@ __device__ __forceinline__ uint4 lds_u4(uint32_t sa) {
 #ifndef SB_ROOT2_TMA
 #define SB_ROOT2_TMA 1
 #endif
+#ifndef SB_ROOT2_EVICT
+#define SB_ROOT2_EVICT 1  // record batches with an L2 evict-first cache hint (0: without, A/B)
+#endif
 __device__ __forceinline__ void mbar_init(uint32_t mb) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
 }
@@ -192,9 +195,19 @@ __device__ __forceinline__ void bulk_batch(uint32_t dst, const void* src, uint32
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the generic reads
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes)
                : "memory");
+#if SB_ROOT2_EVICT
+  // the tree is read once per launch: evict-first in L2, so it does not displace factor rows
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(mb), "l"(pol) : "memory");
+#else
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
       ::"r"(dst), "l"(src), "r"(bytes), "r"(mb) : "memory");
+#endif
 }
 __device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t parity) {
   asm volatile(
