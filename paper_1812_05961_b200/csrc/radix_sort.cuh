@@ -152,10 +152,24 @@ __device__ __forceinline__ void rs_mbar_wait(uint32_t mb, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra RSW%=;\n\t}" ::"r"(mb), "r"(parity) : "memory");
 }
+// SB_RS_EVICT (A/B, profiles/ab_r02/evict/): the once-read tiles with an L2 evict-first cache
+// hint, leaving L2 to the scattered writes of the pass.
+#ifndef SB_RS_EVICT
+#define SB_RS_EVICT 0
+#endif
 __device__ __forceinline__ void rs_bulk(uint32_t dst, const void* src, uint32_t bytes, uint32_t mb) {
+#if SB_RS_EVICT
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(mb), "l"(pol) : "memory");
+#else
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
       ::"r"(dst), "l"(src), "r"(bytes), "r"(mb) : "memory");
+#endif
 }
 
 // Issued by one thread: the first (count & ~3) pairs of tile `tile` into buffer `bk` (keys) /
